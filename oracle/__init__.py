@@ -1,0 +1,180 @@
+"""CPU oracle for Schur-form eigenvalue reordering (ctypes binding of sn_oracle.c).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, ``__graft_entry__.smoke()`` and
+``bench.py``'s cpu_baseline / ``--impl reference`` legs may import this
+package.  It shares no code with ``paper_1905_04975_b200`` (the product), and
+the product never imports it.
+
+Every function is a thin marshalling wrapper around the plain C in
+``sn_oracle.c``; see the header ``sn_oracle.h`` for what each computes and the
+PAPER.md / SPEC.md / SURVEY.md passages it follows.  Matrices are numpy fp64
+arrays in Fortran (column-major) order.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sn_oracle.c")
+_LIB = os.path.join(_HERE, "libsn_oracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile sn_oracle.c with plain gcc (no fast-math, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "sn_oracle.h"))):
+        tmp = _LIB + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fPIC", "-shared",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class Stats(C.Structure):
+    _fields_ = [("windows", C.c_int64), ("swaps", C.c_int64), ("swaps_by_type", C.c_int64 * 4),
+                ("rejected_window", C.c_int64), ("rejected_swap", C.c_int64),
+                ("rejected_row", C.c_int64), ("rejected_n1", C.c_int32), ("rejected_n2", C.c_int32),
+                ("eq_flops", C.c_double)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        d, i64, i32, p = C.c_double, C.c_int64, C.c_int, C.c_void_p
+        pd = C.POINTER(C.c_double)
+        _lib.or_lartg.argtypes = [d, d, pd, pd, pd]
+        _lib.or_larfg3.argtypes = [pd, pd, pd]
+        _lib.or_lanv2.argtypes = [pd, pd, pd, pd, pd, pd]
+        _lib.or_sylv.argtypes = [i32, i32, p, p, p, p, pd]
+        _lib.or_sylv.restype = i32
+        _lib.or_swap.argtypes = [i64, p, i64, i64, i32, i32, p, i64, i64]
+        _lib.or_swap.restype = i32
+        _lib.or_scan.argtypes = [i64, p, i64, p]
+        _lib.or_scan.restype = i32
+        _lib.or_select.argtypes = [i64, p, p, p, C.POINTER(C.c_int64)]
+        _lib.or_schedule.argtypes = [i64, p, p, i64, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                     p, p, p, p, p, p]
+        _lib.or_schedule.restype = i32
+        _lib.or_reorder.argtypes = [i32, i64, p, i64, p, i64, p, C.POINTER(C.c_int64), i64, i64, i64,
+                                    p, C.POINTER(Stats)]
+        _lib.or_reorder.restype = i32
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a):
+    a = np.asarray(a, dtype=np.float64)
+    return np.asfortranarray(a)
+
+
+def lartg(f: float, g: float):
+    c, s, r = C.c_double(), C.c_double(), C.c_double()
+    lib().or_lartg(f, g, C.byref(c), C.byref(s), C.byref(r))
+    return c.value, s.value, r.value
+
+
+def larfg3(alpha: float, x):
+    a = C.c_double(alpha)
+    xx = (C.c_double * 2)(*x)
+    tau = C.c_double()
+    lib().or_larfg3(C.byref(a), xx, C.byref(tau))
+    return a.value, [xx[0], xx[1]], tau.value
+
+
+def lanv2(a, b, c, d):
+    v = [C.c_double(x) for x in (a, b, c, d)]
+    cs, sn = C.c_double(), C.c_double()
+    lib().or_lanv2(*[C.byref(x) for x in v], C.byref(cs), C.byref(sn))
+    return tuple(x.value for x in v) + (cs.value, sn.value)
+
+
+def sylv(T11, T22, T12):
+    """Solve T11 X - X T22 = scale*T12; returns (X, scale, info)."""
+    T11 = np.atleast_2d(np.asarray(T11, float)); T22 = np.atleast_2d(np.asarray(T22, float))
+    T12 = np.atleast_2d(np.asarray(T12, float))
+    n1, n2 = T11.shape[0], T22.shape[0]
+    def pad(a):
+        out = np.zeros((2, 2), order="F"); out[:a.shape[0], :a.shape[1]] = a; return out
+    a, b, c = pad(T11), pad(T22), pad(T12.reshape(n1, n2))
+    X = np.zeros((2, 2), order="F")
+    scale = C.c_double()
+    info = lib().or_sylv(n1, n2, _ptr(a), _ptr(b), _ptr(c), _ptr(X), C.byref(scale))
+    return X[:n1, :n2].copy(), scale.value, info
+
+
+def swap(T, j: int, n1: int, n2: int, Qm=None):
+    """Swap adjacent blocks in place on copies; returns (rc, T', Qm')."""
+    T = _f64(T).copy(order="F")
+    Qc = None if Qm is None else _f64(Qm).copy(order="F")
+    rc = lib().or_swap(T.shape[0], _ptr(T), T.shape[0], j, n1, n2, _ptr(Qc),
+                       0 if Qc is None else Qc.shape[0], 0 if Qc is None else Qc.shape[0])
+    return rc, T, Qc
+
+
+def scan(S):
+    S = _f64(S)
+    n = S.shape[0]
+    bmap = np.zeros(n, np.int8)
+    rc = lib().or_scan(n, _ptr(S), max(n, 1), _ptr(bmap))
+    return rc, bmap
+
+
+def select(bmap, sel):
+    bmap = np.ascontiguousarray(bmap, np.int8)
+    sel = np.ascontiguousarray(sel, np.int32)
+    out = np.zeros(len(bmap), np.int8)
+    m = C.c_int64()
+    lib().or_select(len(bmap), _ptr(bmap), _ptr(sel), _ptr(out), C.byref(m))
+    return out, m.value
+
+
+def schedule(bmap, selrow, w: int):
+    """Window schedule: dict with j1, j2 (per window), off (len nwin+1), and swaps (j, n1, n2)."""
+    bmap = np.ascontiguousarray(bmap, np.int8)
+    selrow = np.ascontiguousarray(selrow, np.int8)
+    n = len(bmap)
+    nw, ns = C.c_int64(), C.c_int64()
+    rc = lib().or_schedule(n, _ptr(bmap), _ptr(selrow), w, C.byref(nw), C.byref(ns),
+                           None, None, None, None, None, None)
+    if rc:
+        raise ValueError("or_schedule rc=%d" % rc)
+    j1 = np.zeros(nw.value, np.int64); j2 = np.zeros(nw.value, np.int64)
+    off = np.zeros(nw.value + 1, np.int64)
+    sj = np.zeros(ns.value, np.int64); s1 = np.zeros(ns.value, np.int8); s2 = np.zeros(ns.value, np.int8)
+    lib().or_schedule(n, _ptr(bmap), _ptr(selrow), w, C.byref(nw), C.byref(ns),
+                      _ptr(j1), _ptr(j2), _ptr(off), _ptr(sj), _ptr(s1), _ptr(s2))
+    return {"j1": j1, "j2": j2, "off": off, "swap_j": sj, "swap_n1": s1, "swap_n2": s2}
+
+
+def reorder(S, Q, select_rows, w: int, mode: int = 1, max_windows: int = -1,
+            force_reject_at: int = -1, inplace: bool = False):
+    """Reorder (Eq. (7)).  mode 1 = accumulated-naive (Fig. 1b), 0 = unblocked (Fig. 1a).
+
+    Returns dict(rc, S, Q, select, m, bmap, stats).  S, Q are Fortran fp64 arrays
+    (copied unless inplace=True and already Fortran fp64)."""
+    if inplace:
+        assert S.dtype == np.float64 and S.flags.f_contiguous
+        Sx = S
+        Qx = Q
+    else:
+        Sx = _f64(S).copy(order="F")
+        Qx = None if Q is None else _f64(Q).copy(order="F")
+    n = Sx.shape[0]
+    sel = np.ascontiguousarray(select_rows, np.int32).copy()
+    m = C.c_int64()
+    bmap = np.zeros(n, np.int8)
+    st = Stats()
+    rc = lib().or_reorder(mode, n, _ptr(Sx), max(n, 1), _ptr(Qx), max(n, 1), _ptr(sel), C.byref(m), w,
+                          max_windows, force_reject_at, _ptr(bmap), C.byref(st))
+    stats = {f: getattr(st, f) for f, _ in Stats._fields_}
+    stats["swaps_by_type"] = list(st.swaps_by_type)
+    return {"rc": rc, "S": Sx, "Q": Qx, "select": sel, "m": m.value, "bmap": bmap, "stats": stats}

@@ -1,0 +1,772 @@
+/*
+ * sn_oracle.c -- CPU oracle for Schur-form eigenvalue reordering.
+ *
+ * TEST INFRASTRUCTURE ONLY (see sn_oracle.h).  Plain, slow, fp64, written to
+ * be checked against the paper by eye:
+ *   - PAPER.md P:84-88, Eq. (7)      the problem  S = Q3 Ŝ Q3^T
+ *   - PAPER.md P:119                 swaps are built from Givens rotations and
+ *                                    3x3 Householder reflectors
+ *   - PAPER.md P:154-158, Fig. 1a/b  scalar vs accumulated (window) updates
+ *   - PAPER.md P:167-184, Fig. 2     chains of windows, W/R/L tasks,
+ *                                    sequentially consistent order
+ * and the readings of SURVEY.md §8c-2..c4 (listed again in DESIGN.md §3),
+ * which fill in what the paper leaves unstated: the swap primitive (the
+ * Bai-Demmel direct swap, restated here in our own code), its sign
+ * conventions, the window schedule, and the stability test.
+ *
+ * No blocking, no fusion, no vectorisation: every update is a scalar loop.
+ */
+#include "sn_oracle.h"
+
+#include <float.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define IDX(a, ld, i, j) ((a)[(i) + (int64_t)(j) * (ld)])
+
+static double dmax(double a, double b) { return a > b ? a : b; }
+static double dmin(double a, double b) { return a < b ? a : b; }
+/* Fortran SIGN(1, x): +1 for x >= +0, -1 for negative x (sign bit). */
+static double sgn1(double x) { return copysign(1.0, x); }
+
+/* sqrt(x^2 + y^2) without destructive underflow/overflow (LAPACK xLAPY2). */
+static double lapy2(double x, double y) {
+  double xa = fabs(x), ya = fabs(y);
+  double w = dmax(xa, ya), z = dmin(xa, ya);
+  if (isnan(x)) return x;
+  if (isnan(y)) return y;
+  if (z == 0.0 || w > DBL_MAX) return w;
+  return w * sqrt(1.0 + (z / w) * (z / w));
+}
+
+/* ---------------------------------------------------------------------------
+ * Givens rotation, SURVEY c4 #2 (LAPACK >= 3.10 xLARTG): c >= 0,
+ * r = sign(f) * hypot(f, g), s = g / r.  g == 0 -> identity; f == 0 ->
+ * (c, s) = (0, sign(g)).
+ * ------------------------------------------------------------------------- */
+void or_lartg(double f, double g, double* c, double* s, double* r) {
+  const double safmin = DBL_MIN, safmax = 1.0 / DBL_MIN;
+  const double rtmin = sqrt(safmin), rtmax = sqrt(safmax / 2.0);
+  double f1 = fabs(f), g1 = fabs(g);
+  if (g == 0.0) {
+    *c = 1.0; *s = 0.0; *r = f;
+  } else if (f == 0.0) {
+    *c = 0.0; *s = sgn1(g); *r = g1;
+  } else if (f1 > rtmin && f1 < rtmax && g1 > rtmin && g1 < rtmax) {
+    double d = sqrt(f * f + g * g);
+    *c = f1 / d;
+    *r = copysign(d, f);
+    *s = g / *r;
+  } else {
+    double u = dmin(safmax, dmax(safmin, dmax(f1, g1)));
+    double fs = f / u, gs = g / u;
+    double d = sqrt(fs * fs + gs * gs);
+    *c = fabs(fs) / d;
+    *r = copysign(d, f);
+    *s = gs / *r;
+    *r *= u;
+  }
+}
+
+/* ---------------------------------------------------------------------------
+ * 3-element Householder reflector, SURVEY c4 #3 (LAPACK xLARFG convention):
+ * beta = -sign(alpha) * ||(alpha, x)||, tau = (beta - alpha) / beta,
+ * v = (1, x / (alpha - beta)).  tau = 0 (H = I) when x == 0.
+ * ------------------------------------------------------------------------- */
+void or_larfg3(double* alpha, double x[2], double* tau) {
+  const double safmin = DBL_MIN / (DBL_EPSILON * 0.5); /* dlamch('S')/dlamch('E') */
+  double xnorm = lapy2(x[0], x[1]);
+  if (xnorm == 0.0) { *tau = 0.0; return; }
+  double beta = -copysign(lapy2(*alpha, xnorm), *alpha);
+  int knt = 0;
+  if (fabs(beta) < safmin) {
+    const double rsafmn = 1.0 / safmin;
+    do {
+      knt++;
+      x[0] *= rsafmn; x[1] *= rsafmn;
+      beta *= rsafmn; *alpha *= rsafmn;
+    } while (fabs(beta) < safmin && knt < 20);
+    xnorm = lapy2(x[0], x[1]);
+    beta = -copysign(lapy2(*alpha, xnorm), *alpha);
+  }
+  *tau = (beta - *alpha) / beta;
+  double sc = 1.0 / (*alpha - beta);
+  x[0] *= sc; x[1] *= sc;
+  for (int i = 0; i < knt; ++i) beta *= safmin;
+  *alpha = beta;
+}
+
+/* ---------------------------------------------------------------------------
+ * Standardisation of a 2x2 block, SURVEY c4 #6 (xLANV2 semantics).
+ * ------------------------------------------------------------------------- */
+void or_lanv2(double* pa, double* pb, double* pc, double* pd, double* pcs, double* psn) {
+  const double eps = DBL_EPSILON;          /* dlamch('P') */
+  const double multpl = 4.0;
+  const double safmn2 = ldexp(1.0, -485);  /* base^(int(log(safmin/eps)/log(base)/2)) */
+  const double safmx2 = 1.0 / safmn2;
+  double a = *pa, b = *pb, c = *pc, d = *pd, cs, sn;
+  if (c == 0.0) {
+    cs = 1.0; sn = 0.0;
+  } else if (b == 0.0) {
+    /* swap rows and columns */
+    cs = 0.0; sn = 1.0;
+    double t = d; d = a; a = t;
+    b = -c; c = 0.0;
+  } else if ((a - d) == 0.0 && sgn1(b) != sgn1(c)) {
+    cs = 1.0; sn = 0.0;   /* already standard, complex pair */
+  } else {
+    double temp = a - d;
+    double p = 0.5 * temp;
+    double bcmax = dmax(fabs(b), fabs(c));
+    double bcmis = dmin(fabs(b), fabs(c)) * sgn1(b) * sgn1(c);
+    double scale = dmax(fabs(p), bcmax);
+    double z = (p / scale) * p + (bcmax / scale) * bcmis;
+    if (z >= multpl * eps) {
+      /* real eigenvalues: compute a and d */
+      z = p + copysign(sqrt(scale) * sqrt(z), p);
+      a = d + z;
+      d = d - (bcmax / z) * bcmis;
+      double tau = lapy2(c, z);
+      cs = z / tau;
+      sn = c / tau;
+      b = b - c;
+      c = 0.0;
+    } else {
+      /* complex, or real (almost) equal eigenvalues: make diagonal equal */
+      int count = 0;
+      double sigma = b + c;
+      for (;;) {
+        count++;
+        scale = dmax(fabs(temp), fabs(sigma));
+        if (scale >= safmx2) {
+          sigma *= safmn2; temp *= safmn2;
+          if (count <= 20) continue;
+        }
+        if (scale <= safmn2) {
+          sigma *= safmx2; temp *= safmx2;
+          if (count <= 20) continue;
+        }
+        break;
+      }
+      p = 0.5 * temp;
+      double tau = lapy2(sigma, temp);
+      cs = sqrt(0.5 * (1.0 + fabs(sigma) / tau));
+      sn = -(p / (tau * cs)) * sgn1(sigma);
+      /* [aa bb; cc dd] = [a b; c d] [cs -sn; sn cs] */
+      double aa = a * cs + b * sn, bb = -a * sn + b * cs;
+      double cc = c * cs + d * sn, dd = -c * sn + d * cs;
+      /* [a b; c d] = [cs sn; -sn cs] [aa bb; cc dd] */
+      a = aa * cs + cc * sn; b = bb * cs + dd * sn;
+      c = -aa * sn + cc * cs; d = -bb * sn + dd * cs;
+      temp = 0.5 * (a + d);
+      a = temp; d = temp;
+      if (c != 0.0) {
+        if (b != 0.0) {
+          if (sgn1(b) == sgn1(c)) {
+            /* real eigenvalues: reduce to upper triangular form */
+            double sab = sqrt(fabs(b)), sac = sqrt(fabs(c));
+            p = copysign(sab * sac, c);
+            tau = 1.0 / sqrt(fabs(b + c));
+            a = temp + p;
+            d = temp - p;
+            b = b - c;
+            c = 0.0;
+            double cs1 = sab * tau, sn1 = sac * tau;
+            temp = cs * cs1 - sn * sn1;
+            sn = cs * sn1 + sn * cs1;
+            cs = temp;
+          }
+        } else {
+          b = -c; c = 0.0;
+          temp = cs; cs = -sn; sn = temp;
+        }
+      }
+    }
+  }
+  *pa = a; *pb = b; *pc = c; *pd = d; *pcs = cs; *psn = sn;
+}
+
+/* ---------------------------------------------------------------------------
+ * Small Sylvester equation T11*X - X*T22 = scale*T12:
+ * Kronecker system K x = scale*vec(T12), K = I (x) T11 - T22^T (x) I, solved by
+ * Gaussian elimination with complete pivoting.  Pivot search scans the active
+ * submatrix column by column (top to bottom) and takes the first strict max.
+ * Pivots below smin = max(eps*max|T|, smlnum) are replaced by smin.
+ * ------------------------------------------------------------------------- */
+int or_sylv(int n1, int n2, const double* T11, const double* T22, const double* T12,
+            double* X, double* scale) {
+  const double eps = DBL_EPSILON, smlnum = DBL_MIN / DBL_EPSILON;
+  const int N = n1 * n2;
+  double K[4][4], rhs[4], y[4];
+  int perm[4];
+  double tmax = 0.0;
+  for (int i = 0; i < n1; ++i)
+    for (int j = 0; j < n1; ++j) tmax = dmax(tmax, fabs(T11[i + 2 * j]));
+  for (int i = 0; i < n2; ++i)
+    for (int j = 0; j < n2; ++j) tmax = dmax(tmax, fabs(T22[i + 2 * j]));
+  const double smin = dmax(eps * tmax, smlnum);
+  /* equation (p,q) <-> row p + n1*q ; unknown X(r,s) <-> column r + n1*s */
+  for (int q = 0; q < n2; ++q)
+    for (int p = 0; p < n1; ++p) {
+      int row = p + n1 * q;
+      rhs[row] = T12[p + 2 * q];
+      for (int s = 0; s < n2; ++s)
+        for (int r = 0; r < n1; ++r) {
+          int col = r + n1 * s;
+          double v = 0.0;
+          if (q == s) v += T11[p + 2 * r];
+          if (p == r) v -= T22[s + 2 * q];
+          K[row][col] = v;
+        }
+    }
+  for (int i = 0; i < N; ++i) perm[i] = i;
+  int info = 0;
+  for (int i = 0; i < N; ++i) {
+    double xmax = -1.0;
+    int ip = i, jp = i;
+    for (int c = i; c < N; ++c)
+      for (int r = i; r < N; ++r)
+        if (fabs(K[r][c]) > xmax) { xmax = fabs(K[r][c]); ip = r; jp = c; }
+    if (ip != i) {
+      for (int c = 0; c < N; ++c) { double t = K[i][c]; K[i][c] = K[ip][c]; K[ip][c] = t; }
+      double t = rhs[i]; rhs[i] = rhs[ip]; rhs[ip] = t;
+    }
+    if (jp != i) {
+      for (int r = 0; r < N; ++r) { double t = K[r][i]; K[r][i] = K[r][jp]; K[r][jp] = t; }
+      int t = perm[i]; perm[i] = perm[jp]; perm[jp] = t;
+    }
+    if (fabs(K[i][i]) < smin) { K[i][i] = smin; info = 1; }
+    for (int r = i + 1; r < N; ++r) {
+      double l = K[r][i] / K[i][i];
+      K[r][i] = 0.0;
+      for (int c = i + 1; c < N; ++c) K[r][c] -= l * K[i][c];
+      rhs[r] -= l * rhs[i];
+    }
+  }
+  /* overflow guard: scale the right-hand side down if a division could overflow */
+  *scale = 1.0;
+  double bmax = 0.0;
+  for (int i = 0; i < N; ++i) bmax = dmax(bmax, fabs(rhs[i]));
+  for (int i = 0; i < N; ++i) {
+    if ((8.0 * smlnum) * fabs(rhs[i]) > fabs(K[i][i])) {
+      *scale = 0.125 / bmax;
+      for (int r = 0; r < N; ++r) rhs[r] *= *scale;
+      break;
+    }
+  }
+  for (int i = N - 1; i >= 0; --i) {
+    double t = rhs[i];
+    for (int c = i + 1; c < N; ++c) t -= K[i][c] * y[c];
+    y[i] = t / K[i][i];
+  }
+  for (int i = 0; i < N; ++i) {
+    int u = perm[i];
+    int r = u % n1, s = u / n1;
+    X[r + 2 * s] = y[i];
+  }
+  return info;
+}
+
+/* ---- plain application of a reflector / rotation to parts of a matrix ---- */
+
+/* rows r0..r0+2, columns c0..c1-1:  A <- (I - tau v v^T) A */
+static void refl_left(double* A, int64_t lda, int64_t r0, int64_t c0, int64_t c1,
+                      const double v[3], double tau) {
+  if (tau == 0.0) return;
+  double t0 = tau * v[0], t1 = tau * v[1], t2 = tau * v[2];
+  for (int64_t c = c0; c < c1; ++c) {
+    double* a = &IDX(A, lda, r0, c);
+    double sum = v[0] * a[0] + v[1] * a[1] + v[2] * a[2];
+    a[0] -= sum * t0;
+    a[1] -= sum * t1;
+    a[2] -= sum * t2;
+  }
+}
+
+/* columns c0..c0+2, rows r0..r1-1:  A <- A (I - tau v v^T) */
+static void refl_right(double* A, int64_t lda, int64_t c0, int64_t r0, int64_t r1,
+                       const double v[3], double tau) {
+  if (tau == 0.0) return;
+  double t0 = tau * v[0], t1 = tau * v[1], t2 = tau * v[2];
+  double* a0 = &IDX(A, lda, 0, c0);
+  double* a1 = &IDX(A, lda, 0, c0 + 1);
+  double* a2 = &IDX(A, lda, 0, c0 + 2);
+  for (int64_t r = r0; r < r1; ++r) {
+    double sum = v[0] * a0[r] + v[1] * a1[r] + v[2] * a2[r];
+    a0[r] -= sum * t0;
+    a1[r] -= sum * t1;
+    a2[r] -= sum * t2;
+  }
+}
+
+/* rows r0, r0+1, columns c0..c1-1:  x' = c x + s y, y' = c y - s x */
+static void rot_left(double* A, int64_t lda, int64_t r0, int64_t c0, int64_t c1, double c, double s) {
+  for (int64_t k = c0; k < c1; ++k) {
+    double x = IDX(A, lda, r0, k), y = IDX(A, lda, r0 + 1, k);
+    IDX(A, lda, r0, k) = c * x + s * y;
+    IDX(A, lda, r0 + 1, k) = c * y - s * x;
+  }
+}
+
+/* columns c0, c0+1, rows r0..r1-1: same formulas on column pairs */
+static void rot_right(double* A, int64_t lda, int64_t c0, int64_t r0, int64_t r1, double c, double s) {
+  double* x = &IDX(A, lda, 0, c0);
+  double* y = &IDX(A, lda, 0, c0 + 1);
+  for (int64_t k = r0; k < r1; ++k) {
+    double xv = x[k], yv = y[k];
+    x[k] = c * xv + s * yv;
+    y[k] = c * yv - s * xv;
+  }
+}
+
+/* ---------------------------------------------------------------------------
+ * Adjacent block swap.
+ * ------------------------------------------------------------------------- */
+int or_swap(int64_t nt, double* T, int64_t ldt, int64_t j, int n1, int n2,
+            double* Qm, int64_t ldq, int64_t nq) {
+  const int nd = n1 + n2;
+  if (n1 == 1 && n2 == 1) {
+    /* Givens rotation from (t12, t22 - t11); the diagonal entries are swapped
+     * exactly and t12 is left untouched. */
+    double t11 = IDX(T, ldt, j, j), t22 = IDX(T, ldt, j + 1, j + 1);
+    double c, s, r;
+    or_lartg(IDX(T, ldt, j, j + 1), t22 - t11, &c, &s, &r);
+    rot_left(T, ldt, j, j + 2, nt, c, s);
+    rot_right(T, ldt, j, 0, j, c, s);
+    IDX(T, ldt, j, j) = t22;
+    IDX(T, ldt, j + 1, j + 1) = t11;
+    if (Qm) rot_right(Qm, ldq, j, 0, nq, c, s);
+    return 0;
+  }
+
+  /* D = the (n1+n2)x(n1+n2) diagonal block, column-major, ld 4 */
+  double D[16];
+  memset(D, 0, sizeof(D));
+  double dnorm = 0.0;
+  for (int c = 0; c < nd; ++c)
+    for (int r = 0; r < nd; ++r) {
+      D[r + 4 * c] = IDX(T, ldt, j + r, j + c);
+      dnorm = dmax(dnorm, fabs(D[r + 4 * c]));
+    }
+  const double eps = DBL_EPSILON, smlnum = DBL_MIN / DBL_EPSILON;
+  const double thresh = dmax(10.0 * eps * dnorm, smlnum);
+
+  /* T11 X - X T22 = scale T12 */
+  double T11[4] = {0}, T22[4] = {0}, T12[4] = {0}, X[4] = {0}, scale;
+  for (int c = 0; c < n1; ++c)
+    for (int r = 0; r < n1; ++r) T11[r + 2 * c] = D[r + 4 * c];
+  for (int c = 0; c < n2; ++c)
+    for (int r = 0; r < n2; ++r) T22[r + 2 * c] = D[(n1 + r) + 4 * (n1 + c)];
+  for (int c = 0; c < n2; ++c)
+    for (int r = 0; r < n1; ++r) T12[r + 2 * c] = D[r + 4 * (n1 + c)];
+  or_sylv(n1, n2, T11, T22, T12, X, &scale);
+
+  /* reflector(s) mapping span[-X; scale*I] onto the leading n2 coordinates */
+  double v1[3], v2[3] = {0, 0, 0}, tau1, tau2 = 0.0;
+  int nrefl;
+  if (n1 == 1) {
+    /* n2 == 2: the complement (scale, X11, X12) goes to the last coordinate */
+    double alpha = X[0 + 2 * 1], x[2] = {scale, X[0]};
+    or_larfg3(&alpha, x, &tau1);
+    v1[0] = x[0]; v1[1] = x[1]; v1[2] = 1.0;
+    nrefl = 1;
+  } else if (n2 == 1) {
+    double alpha = -X[0], x[2] = {-X[1], scale};
+    or_larfg3(&alpha, x, &tau1);
+    v1[0] = 1.0; v1[1] = x[0]; v1[2] = x[1];
+    nrefl = 1;
+  } else {
+    double alpha = -X[0], x[2] = {-X[1], scale};
+    or_larfg3(&alpha, x, &tau1);
+    v1[0] = 1.0; v1[1] = x[0]; v1[2] = x[1];
+    /* image of the second column of [-X; scale*I] under H1, rows 2..4 */
+    double temp = -tau1 * (X[0 + 2 * 1] + v1[1] * X[1 + 2 * 1]);
+    double alpha2 = -temp * v1[1] - X[1 + 2 * 1];
+    double x2[2] = {-temp * v1[2], scale};
+    or_larfg3(&alpha2, x2, &tau2);
+    v2[0] = 1.0; v2[1] = x2[0]; v2[2] = x2[1];
+    nrefl = 2;
+  }
+
+  /* trial on D */
+  double Dn[16];
+  memcpy(Dn, D, sizeof(D));
+  if (nrefl == 1) {
+    refl_left(Dn, 4, 0, 0, nd, v1, tau1);
+    refl_right(Dn, 4, 0, 0, nd, v1, tau1);
+  } else {
+    refl_left(Dn, 4, 0, 0, 4, v1, tau1);
+    refl_right(Dn, 4, 0, 0, 4, v1, tau1);
+    refl_left(Dn, 4, 1, 0, 4, v2, tau2);
+    refl_right(Dn, 4, 1, 0, 4, v2, tau2);
+  }
+
+  /* weak stability test */
+  double resid;
+  if (n1 == 1) {        /* (1,2): old 1x1 now at position 2 */
+    resid = dmax(dmax(fabs(Dn[2 + 4 * 0]), fabs(Dn[2 + 4 * 1])), fabs(Dn[2 + 4 * 2] - D[0]));
+  } else if (n2 == 1) { /* (2,1): old 1x1 now at position 0 */
+    resid = dmax(dmax(fabs(Dn[1 + 4 * 0]), fabs(Dn[2 + 4 * 0])), fabs(Dn[0] - D[2 + 4 * 2]));
+  } else {
+    resid = dmax(dmax(fabs(Dn[2 + 4 * 0]), fabs(Dn[2 + 4 * 1])),
+                 dmax(fabs(Dn[3 + 4 * 0]), fabs(Dn[3 + 4 * 1])));
+  }
+  if (!(resid <= thresh)) return 1;
+
+  /* exact zeros below the new blocks and the exact moved 1x1 eigenvalue (c4 #7) */
+  if (n1 == 1) {
+    Dn[2 + 4 * 0] = 0.0; Dn[2 + 4 * 1] = 0.0; Dn[2 + 4 * 2] = D[0];
+  } else if (n2 == 1) {
+    Dn[0] = D[2 + 4 * 2]; Dn[1 + 4 * 0] = 0.0; Dn[2 + 4 * 0] = 0.0;
+  } else {
+    Dn[2 + 4 * 0] = 0.0; Dn[2 + 4 * 1] = 0.0; Dn[3 + 4 * 0] = 0.0; Dn[3 + 4 * 1] = 0.0;
+  }
+
+  /* re-standardise each moved 2x2 block; a block that would split (real
+   * eigenvalues) is a structure change and the swap is rejected. */
+  double rc[2] = {1, 1}, rs[2] = {0, 0};
+  int rpos[2] = {-1, -1};
+  int nrot = 0;
+  if (n2 == 2) rpos[nrot++] = 0;
+  if (n1 == 2) rpos[nrot++] = n2;
+  for (int q = 0; q < nrot; ++q) {
+    int p = rpos[q];
+    double a = Dn[p + 4 * p], b = Dn[p + 4 * (p + 1)], c = Dn[(p + 1) + 4 * p], d = Dn[(p + 1) + 4 * (p + 1)];
+    double cs, sn;
+    or_lanv2(&a, &b, &c, &d, &cs, &sn);
+    if (c == 0.0) return 1;
+    Dn[p + 4 * p] = a; Dn[p + 4 * (p + 1)] = b; Dn[(p + 1) + 4 * p] = c; Dn[(p + 1) + 4 * (p + 1)] = d;
+    rot_left(Dn, 4, p, p + 2, nd, cs, sn);
+    rot_right(Dn, 4, p, 0, p, cs, sn);
+    rc[q] = cs; rs[q] = sn;
+  }
+
+  /* commit: rows j..j+nd-1 right of the block, columns j..j+nd-1 above it, Qm */
+  if (nrefl == 1) {
+    refl_left(T, ldt, j, j + nd, nt, v1, tau1);
+    refl_right(T, ldt, j, 0, j, v1, tau1);
+    if (Qm) refl_right(Qm, ldq, j, 0, nq, v1, tau1);
+  } else {
+    refl_left(T, ldt, j, j + nd, nt, v1, tau1);
+    refl_left(T, ldt, j + 1, j + nd, nt, v2, tau2);
+    refl_right(T, ldt, j, 0, j, v1, tau1);
+    refl_right(T, ldt, j + 1, 0, j, v2, tau2);
+    if (Qm) {
+      refl_right(Qm, ldq, j, 0, nq, v1, tau1);
+      refl_right(Qm, ldq, j + 1, 0, nq, v2, tau2);
+    }
+  }
+  for (int q = 0; q < nrot; ++q) {
+    int64_t p = j + rpos[q];
+    rot_left(T, ldt, p, j + nd, nt, rc[q], rs[q]);
+    rot_right(T, ldt, p, 0, j, rc[q], rs[q]);
+    if (Qm) rot_right(Qm, ldq, p, 0, nq, rc[q], rs[q]);
+  }
+  for (int c = 0; c < nd; ++c)
+    for (int r = 0; r < nd; ++r) IDX(T, ldt, j + r, j + c) = Dn[r + 4 * c];
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * Structure ("upper quasi-triangular with 1x1 and 2x2 blocks").
+ * ------------------------------------------------------------------------- */
+int or_scan(int64_t n, const double* S, int64_t lds, int8_t* bmap) {
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = j + 2; i < n; ++i)
+      if (IDX(S, lds, i, j) != 0.0) return -2;
+  int64_t i = 0;
+  while (i < n) {
+    if (i + 1 < n && IDX(S, lds, i + 1, i) != 0.0) {
+      if (i + 2 < n && IDX(S, lds, i + 2, i + 1) != 0.0) return -2;
+      bmap[i] = 1; bmap[i + 1] = 2; i += 2;
+    } else {
+      bmap[i] = 0; i += 1;
+    }
+  }
+  return 0;
+}
+
+void or_select(int64_t n, const int8_t* bmap, const int32_t* select, int8_t* selrow, int64_t* m) {
+  int64_t cnt = 0;
+  for (int64_t i = 0; i < n;) {
+    if (bmap[i] == 1) {
+      int8_t s = (select[i] != 0 || select[i + 1] != 0) ? 1 : 0;
+      selrow[i] = s; selrow[i + 1] = s;
+      cnt += 2 * s;
+      i += 2;
+    } else {
+      selrow[i] = select[i] != 0 ? 1 : 0;
+      cnt += selrow[i];
+      i += 1;
+    }
+  }
+  *m = cnt;
+}
+
+/* ---------------------------------------------------------------------------
+ * Window schedule.  The block list evolves as windows are
+ * executed; the schedule only depends on block sizes and selection flags.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t B, w, ks, placed;
+  int8_t* bsz;     /* block sizes, current order */
+  int8_t* bsel;    /* selection flags, current order */
+  int64_t* brow;   /* first row of each block */
+  int in_chain;    /* 1 while following a chain upward */
+  int64_t bottom;  /* block index one past the movers of the current chain */
+  int64_t nmov;    /* movers of the current chain */
+} sched_t;
+
+static int sched_init(sched_t* st, int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w) {
+  memset(st, 0, sizeof(*st));
+  st->bsz = (int8_t*)malloc((size_t)(n + 1));
+  st->bsel = (int8_t*)malloc((size_t)(n + 1));
+  st->brow = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  if (!st->bsz || !st->bsel || !st->brow) return -1;
+  int64_t B = 0;
+  for (int64_t i = 0; i < n;) {
+    int sz = bmap[i] == 1 ? 2 : 1;
+    st->bsz[B] = (int8_t)sz;
+    st->bsel[B] = selrow[i];
+    st->brow[B] = i;
+    B++;
+    i += sz;
+  }
+  st->B = B; st->w = w; st->ks = w / 2; st->placed = 0; st->in_chain = 0;
+  return 0;
+}
+
+static void sched_free(sched_t* st) {
+  free(st->bsz); free(st->bsel); free(st->brow);
+}
+
+/* Next non-empty window.  Appends its swaps (global row j, n1, n2) to the
+ * callback buffers via sw_* arrays of capacity cap (may be NULL) and returns
+ * the number of swaps; returns -1 when the schedule is complete. */
+static int64_t sched_next(sched_t* st, int64_t* j1, int64_t* j2,
+                          int64_t* sw_j, int8_t* sw_n1, int8_t* sw_n2) {
+  for (;;) {
+    if (!st->in_chain) {
+      /* (a) G = longest prefix of the unplaced selected blocks with <= ks rows */
+      int64_t f = st->placed;
+      while (f < st->B && !st->bsel[f]) f++;
+      if (f >= st->B) return -1;
+      int64_t rows = 0, cnt = 0, last = -1;
+      for (int64_t b = f; b < st->B; ++b) {
+        if (!st->bsel[b]) continue;
+        if (cnt > 0 && rows + st->bsz[b] > st->ks) break;
+        rows += st->bsz[b]; cnt++; last = b;
+      }
+      /* (b) already contiguous at `placed`: nothing to move */
+      if (f == st->placed && last == st->placed + cnt - 1) {
+        st->placed += cnt;
+        continue;
+      }
+      /* (c) */
+      st->bottom = last + 1;
+      st->nmov = cnt;
+      st->in_chain = 1;
+    }
+    /* (d) top = smallest block index >= placed with rows(top..bottom) <= w */
+    int64_t top = st->bottom, rw = 0;
+    while (top > st->placed && rw + st->bsz[top - 1] <= st->w) { top--; rw += st->bsz[top]; }
+    int64_t wj1 = st->brow[top], wj2 = wj1 + rw;
+    /* (e) movers in top-to-bottom order; mover i ends at block top+i */
+    int64_t nsw = 0, im = 0;
+    for (int64_t b = top; b < st->bottom; ++b) {
+      if (!st->bsel[b]) continue;
+      int64_t tgt = top + im;
+      for (int64_t q = b; q > tgt; --q) {
+        if (sw_j) { sw_j[nsw] = st->brow[q - 1]; sw_n1[nsw] = st->bsz[q - 1]; sw_n2[nsw] = st->bsz[q]; }
+        nsw++;
+        int8_t tsz = st->bsz[q - 1], tsel = st->bsel[q - 1];
+        st->bsz[q - 1] = st->bsz[q]; st->bsel[q - 1] = st->bsel[q];
+        st->bsz[q] = tsz; st->bsel[q] = tsel;
+        st->brow[q] = st->brow[q - 1] + st->bsz[q - 1];
+      }
+      im++;
+    }
+    /* (f) */
+    if (top == st->placed) {
+      st->placed = top + im;
+      st->in_chain = 0;
+    } else {
+      st->bottom = top + im;
+    }
+    if (nsw > 0) { *j1 = wj1; *j2 = wj2; return nsw; }
+  }
+}
+
+/* Upper bound on the swaps of one window: a mover passes each other block at most once. */
+static int64_t max_swaps_per_window(int64_t w) { return (w * w) / 4 + w + 4; }
+
+int or_schedule(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w,
+                int64_t* nwin, int64_t* nswap,
+                int64_t* win_j1, int64_t* win_j2, int64_t* swap_off,
+                int64_t* swap_j, int8_t* swap_n1, int8_t* swap_n2) {
+  if (w < 4) return -4;
+  sched_t st;
+  if (sched_init(&st, n, bmap, selrow, w)) return -100;
+  int64_t cap = max_swaps_per_window(w);
+  int64_t* tj = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
+  int8_t* t1 = (int8_t*)malloc((size_t)cap);
+  int8_t* t2 = (int8_t*)malloc((size_t)cap);
+  int64_t nw = 0, ns = 0, j1, j2, k;
+  while ((k = sched_next(&st, &j1, &j2, tj, t1, t2)) >= 0) {
+    if (win_j1) {
+      win_j1[nw] = j1; win_j2[nw] = j2; swap_off[nw] = ns;
+      for (int64_t i = 0; i < k; ++i) { swap_j[ns + i] = tj[i]; swap_n1[ns + i] = t1[i]; swap_n2[ns + i] = t2[i]; }
+    }
+    nw++; ns += k;
+  }
+  if (win_j1) swap_off[nw] = ns;
+  *nwin = nw; *nswap = ns;
+  free(tj); free(t1); free(t2);
+  sched_free(&st);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * The reordering, Eq. (7).
+ * ------------------------------------------------------------------------- */
+static void window_updates_naive(int64_t n, double* S, int64_t lds, double* Q, int64_t ldq,
+                                 int64_t j1, int64_t j2, const double* Z) {
+  const int64_t k = j2 - j1;
+  double* tmp = (double*)malloc(sizeof(double) * (size_t)k);
+  /* left update: S[j1:j2, j2:n] <- Z^T S[j1:j2, j2:n] */
+  for (int64_t c = j2; c < n; ++c) {
+    for (int64_t r = 0; r < k; ++r) {
+      double acc = 0.0;
+      for (int64_t l = 0; l < k; ++l) acc += Z[l + r * k] * IDX(S, lds, j1 + l, c);
+      tmp[r] = acc;
+    }
+    for (int64_t r = 0; r < k; ++r) IDX(S, lds, j1 + r, c) = tmp[r];
+  }
+  /* right update: S[0:j1, j1:j2] <- S[0:j1, j1:j2] Z */
+  for (int64_t r = 0; r < j1; ++r) {
+    for (int64_t c = 0; c < k; ++c) {
+      double acc = 0.0;
+      for (int64_t l = 0; l < k; ++l) acc += IDX(S, lds, r, j1 + l) * Z[l + c * k];
+      tmp[c] = acc;
+    }
+    for (int64_t c = 0; c < k; ++c) IDX(S, lds, r, j1 + c) = tmp[c];
+  }
+  /* Q update (Q <- Q Q3): Q[:, j1:j2] <- Q[:, j1:j2] Z */
+  if (Q) {
+    for (int64_t r = 0; r < n; ++r) {
+      for (int64_t c = 0; c < k; ++c) {
+        double acc = 0.0;
+        for (int64_t l = 0; l < k; ++l) acc += IDX(Q, ldq, r, j1 + l) * Z[l + c * k];
+        tmp[c] = acc;
+      }
+      for (int64_t c = 0; c < k; ++c) IDX(Q, ldq, r, j1 + c) = tmp[c];
+    }
+  }
+  free(tmp);
+}
+
+int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t ldq,
+               int32_t* select, int64_t* m, int64_t w, int64_t max_windows,
+               int64_t force_reject_at, int8_t* bmap_out, or_stats* st) {
+  if (mode != 0 && mode != 1) return -1;
+  if (n < 0) return -2;
+  if (n > 0 && S == NULL) return -3;
+  if (lds < (n > 1 ? n : 1)) return -4;
+  if (Q && ldq < (n > 1 ? n : 1)) return -6;
+  if (n > 0 && select == NULL) return -7;
+  if (m == NULL) return -8;
+  if (w < 4) return -9;
+  or_stats local;
+  if (!st) st = &local;
+  memset(st, 0, sizeof(*st));
+  st->rejected_window = -1; st->rejected_swap = -1; st->rejected_row = -1;
+  *m = 0;
+  if (n == 0) return 0;
+
+  int8_t* bmap = (int8_t*)malloc((size_t)n);
+  int8_t* selrow = (int8_t*)malloc((size_t)n);
+  if (or_scan(n, S, lds, bmap)) { free(bmap); free(selrow); return -3; }
+  or_select(n, bmap, select, selrow, m);
+
+  sched_t sc;
+  sched_init(&sc, n, bmap, selrow, w);
+  int64_t cap = max_swaps_per_window(w);
+  int64_t* tj = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
+  int8_t* t1 = (int8_t*)malloc((size_t)cap);
+  int8_t* t2 = (int8_t*)malloc((size_t)cap);
+  double* D = (double*)malloc(sizeof(double) * (size_t)w * (size_t)w);
+  double* Z = (double*)malloc(sizeof(double) * (size_t)w * (size_t)w);
+  int rc = 0;
+  int64_t j1, j2, k, gswap = 0;
+  while ((max_windows < 0 || st->windows < max_windows) &&
+         (k = sched_next(&sc, &j1, &j2, tj, t1, t2)) >= 0) {
+    const int64_t kw = j2 - j1;
+    int64_t done = 0;
+    if (mode == 0) {
+      for (; done < k; ++done) {
+        if (gswap + done == force_reject_at ||
+            or_swap(n, S, lds, tj[done], t1[done], t2[done], Q, ldq, Q ? n : 0)) {
+          rc = 1; break;
+        }
+        st->swaps_by_type[(t1[done] - 1) * 2 + (t2[done] - 1)]++;
+      }
+    } else {
+      for (int64_t c = 0; c < kw; ++c)
+        for (int64_t r = 0; r < kw; ++r) {
+          D[r + c * kw] = IDX(S, lds, j1 + r, j1 + c);
+          Z[r + c * kw] = (r == c) ? 1.0 : 0.0;
+        }
+      for (; done < k; ++done) {
+        if (gswap + done == force_reject_at ||
+            or_swap(kw, D, kw, tj[done] - j1, t1[done], t2[done], Z, kw, kw)) {
+          rc = 1; break;
+        }
+        st->swaps_by_type[(t1[done] - 1) * 2 + (t2[done] - 1)]++;
+      }
+      for (int64_t c = 0; c < kw; ++c)
+        for (int64_t r = 0; r < kw; ++r) IDX(S, lds, j1 + r, j1 + c) = D[r + c * kw];
+      window_updates_naive(n, S, lds, Q, ldq, j1, j2, Z);
+    }
+    st->swaps += done;
+    st->windows++;
+    st->eq_flops += 2.0 * kw * kw * ((double)(n - j2) + (double)j1 + (Q ? (double)n : 0.0));
+    if (rc) {
+      st->rejected_window = st->windows - 1;
+      st->rejected_swap = gswap + done;
+      st->rejected_row = tj[done];
+      st->rejected_n1 = t1[done];
+      st->rejected_n2 = t2[done];
+      /* roll the block list back to the state reached: undo the swaps of this
+       * window that sched_next performed symbolically but were not executed */
+      for (int64_t i = k - 1; i >= done; --i) {
+        /* the swap exchanged blocks at rows tj[i] (size t1) and tj[i]+t1 (size t2);
+         * after it the block of size t2 is at row tj[i].  Find its index. */
+        int64_t lo = 0, hi = sc.B - 1, b = -1;
+        while (lo <= hi) {
+          int64_t mid = (lo + hi) / 2;
+          if (sc.brow[mid] == tj[i]) { b = mid; break; }
+          if (sc.brow[mid] < tj[i]) lo = mid + 1; else hi = mid - 1;
+        }
+        int8_t tsz = sc.bsz[b], tsel = sc.bsel[b];
+        sc.bsz[b] = sc.bsz[b + 1]; sc.bsel[b] = sc.bsel[b + 1];
+        sc.bsz[b + 1] = tsz; sc.bsel[b + 1] = tsel;
+        sc.brow[b + 1] = sc.brow[b] + sc.bsz[b];
+      }
+      break;
+    }
+    gswap += k;
+  }
+  /* achieved selection mask and block map */
+  for (int64_t b = 0; b < sc.B; ++b) {
+    int64_t r = sc.brow[b];
+    for (int q = 0; q < sc.bsz[b]; ++q) {
+      select[r + q] = sc.bsel[b];
+      if (bmap_out) bmap_out[r + q] = (int8_t)(sc.bsz[b] == 1 ? 0 : 1 + q);
+    }
+  }
+  free(tj); free(t1); free(t2); free(D); free(Z);
+  free(bmap); free(selrow);
+  sched_free(&sc);
+  return rc;
+}
