@@ -1,0 +1,121 @@
+/*
+ * sn_reorder.h -- C ABI of libsn_b200.so, a B200-native (sm_100a) implementation of the
+ * eigenvalue-reordering step of StarNEig (arXiv 1905.04975).
+ *
+ * The operation (Eq. (7)): given a real Schur form S (upper
+ * quasi-triangular with 1x1 and 2x2 diagonal blocks) and Schur vectors Q, compute an
+ * orthogonal Q3 with  S = Q3 Ŝ Q3^T  such that the selected eigenvalues appear in the
+ * leading diagonal blocks of Ŝ; overwrite S <- Ŝ and Q <- Q*Q3.
+ *
+ * The method: chains of diagonal windows of at most w rows.  The
+ * window task applies adjacent 1x1/2x2 block swaps (Givens rotations and 3x3 Householder
+ * reflectors) to the diagonal window and accumulates them into a k x k orthogonal
+ * Z; right/left update tasks apply Z with level-3 (here FP64 tensor-core DMMA) products
+ * to the column panel above the window, the row panel to its right and the columns of Q.
+ * Readings of what the paper leaves unstated (window schedule, swap conventions,
+ * stability test) are listed in DESIGN.md §3.
+ *
+ * Conventions for every entry point:
+ *   - matrices are FP64, column-major, element (i,j) at a[i + j*ld], 0-based;
+ *   - S and Q may be DEVICE pointers (cudaMalloc / torch CUDA tensors: the fast path) or
+ *     HOST pointers (pageable or pinned; staged through device memory inside the call);
+ *   - the caller owns every buffer; S and Q are modified in place (LAPACK style);
+ *   - `select` is a HOST int32 array of n entries, one per row: nonzero = selected.  A
+ *     2x2 block is selected if either of its rows is (LAPACK DTRSEN convention).
+ *     On return it holds the achieved per-row mask (1 for rows < m after a full run);
+ *   - return codes (LAPACK INFO style): 0 success; -i argument i invalid (n < 0, null
+ *     pointer, ld too small, -2 also when S is not upper quasi-triangular); SN_ERR_REJECTED
+ *     (+1) a block swap failed the stability test: S and Q hold a valid, partially
+ *     reordered Schur form and select/m describe it; SN_ERR_CUDA (+2) a CUDA error;
+ *     SN_ERR_UNSUPPORTED (+4) an option outside the supported range.
+ *   - No CPU fallback: every arithmetic step runs in the library's CUDA kernels.  Without
+ *     a usable CUDA device the compute entry points return SN_ERR_CUDA.
+ */
+#ifndef SN_REORDER_H
+#define SN_REORDER_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SN_OK 0
+#define SN_ERR_REJECTED 1
+#define SN_ERR_CUDA 2
+#define SN_ERR_UNSUPPORTED 4
+
+/* Options (sn_default_opts fills the defaults). */
+typedef struct sn_opts {
+  int64_t window;            /* w: maximum window rows, 4 <= w <= 256 (default 256).
+                                SURVEY §8c-2: ks = w/2 rows of movers per chain group. */
+  int64_t inner_window;      /* rows of the in-kernel inner windows (default 64, <= 64) */
+  int64_t max_windows;       /* stop after this many windows (prefix runs); < 0 = all */
+  int64_t force_reject_window; /* debug: window (schedule order) whose swap is rejected */
+  int64_t force_reject_swap;   /* debug: swap index (execution order within that window) */
+  int32_t validate_lower;    /* 1: also check that S is exactly 0 below the subdiagonal
+                                (n^2/2 device reads); the subdiagonal is always checked */
+  int32_t serialize;         /* 1: debug, synchronise after every launch */
+  int32_t q_stream_overlap;  /* 1 (default): Q updates on a second stream, overlapping the
+                                next level's window tasks */
+  int32_t reserved;
+} sn_opts;
+
+/* Statistics of one call. */
+typedef struct sn_stats {
+  int64_t windows;           /* windows executed */
+  int64_t levels;            /* dependency levels of the window DAG */
+  int64_t swaps;             /* block swaps scheduled in executed windows */
+  int64_t swaps_by_type[4];  /* index (n1-1)*2 + (n2-1) */
+  int64_t inner_windows;     /* in-kernel inner windows */
+  int64_t rejected_window;   /* -1 if none */
+  int64_t rejected_row;      /* first row j of the rejected swap (blocks n1 at j, n2 at j+n1) */
+  int32_t rejected_n1, rejected_n2;
+  double eq_flops;           /* equivalent update flops: per window with >= 1
+                                swap, 2k^2 (n - j2) + 2k^2 j1 + 2k^2 n (Q term only if Q) */
+  double ms_schedule;        /* host: structure scan + schedule construction */
+  double ms_device;          /* device time of the reordering (CUDA events) */
+  double ms_total;           /* wall time of the call */
+  double ms_h2d, ms_d2h;     /* host-pointer staging copies (0 for device pointers) */
+} sn_stats;
+
+void sn_default_opts(sn_opts* o);
+const char* sn_strerror(int code);
+
+/* Eq. (7) with default options.  n: order; S (n x n, ld ldS >= max(1,n)); Q (n x n, ldQ >=
+ * max(1,n)) or NULL (do not accumulate, LAPACK COMPQ='N'); select: host int32[n] in/out;
+ * m: out, number of selected rows.  Synchronous with respect to the host. */
+int sn_reorder_schur(int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ,
+                     int32_t* select, int64_t* m);
+
+/* Same with options, an optional host int8[n] block map output (0 = 1x1 block, 1/2 = first
+ * and second row of a 2x2 block), optional statistics, and a CUDA stream (cudaStream_t, or
+ * NULL for the legacy default stream) on which the device work is ordered.  Still
+ * synchronous with respect to the host on return. */
+int sn_reorder_schur_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS, double* Q,
+                        int64_t ldQ, int32_t* select, int64_t* m, int8_t* bmap_out,
+                        sn_stats* stats, void* stream);
+
+/* ---- host-only helpers (no GPU needed): the window schedule of SURVEY §8c-2 ----
+ * From a block map (bmap as above) and a per-row selection (0/1, block consistent),
+ * sn_schedule_build computes the windows the library executes, in schedule order:
+ * win_j1[t], win_k[t] (rows [j1, j1+k)), win_level[t] (its dependency level) and
+ * win_nswap[t].  Pass NULL arrays to query only *nwin and *nswap.  Returns 0 or -i. */
+int sn_schedule_build(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w,
+                      int64_t* nwin, int64_t* nswap, int64_t* nlevels,
+                      int64_t* win_j1, int64_t* win_k, int64_t* win_level, int64_t* win_nswap);
+
+/* The swaps of window t of the schedule above, in the library's execution order inside
+ * the window (inner windows of `inner_window` rows): global row j, sizes n1 (block at j),
+ * n2 (moving block at j+n1).  cap = capacity of the arrays; returns the number of swaps or
+ * a negative error. */
+int64_t sn_schedule_window_swaps(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w,
+                                 int64_t inner_window, int64_t t, int64_t cap,
+                                 int64_t* swap_j, int8_t* swap_n1, int8_t* swap_n2);
+
+/* Library version string. */
+const char* sn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

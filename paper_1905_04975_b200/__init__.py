@@ -1,0 +1,191 @@
+"""B200-native eigenvalue reordering of a real Schur form (arXiv 1905.04975, Eq. (7)).
+
+Thin ctypes binding of ``libsn_b200.so`` (C ABI: ``include/sn_reorder.h``).  Argument
+marshalling only: every step of the reordering runs in the library's CUDA kernels.  There
+is no CPU fallback -- if the shared library is missing, importing this package raises.
+
+Matrices are passed as torch tensors whose memory is the column-major matrix, i.e. a
+contiguous row-major tensor ``T`` with ``T[j, i] == S[i, j]`` (see ``workloads``), either
+on ``cuda`` (fast path, in place) or on the CPU (staged through the GPU inside the call).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+LIB_PATH = os.path.join(_HERE, "libsn_b200.so")
+CSRC = os.path.join(_HERE, "csrc")
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+
+
+def sources():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile the CUDA library for sm_100a (nvcc; works without a GPU)."""
+    srcs = sources()
+    deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    deps.append(os.path.join(_ROOT, "include", "sn_reorder.h"))
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= max(map(os.path.getmtime, deps)):
+        return LIB_PATH
+    tmp = LIB_PATH + ".tmp%d" % os.getpid()
+    cmd = ["nvcc", *NVCC_FLAGS, "-shared", "-I", os.path.join(_ROOT, "include"), "-o", tmp, *srcs]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + out.stderr[-6000:])
+    if verbose:
+        print(out.stderr)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+class Opts(C.Structure):
+    _fields_ = [("window", C.c_int64), ("inner_window", C.c_int64), ("max_windows", C.c_int64),
+                ("force_reject_window", C.c_int64), ("force_reject_swap", C.c_int64),
+                ("validate_lower", C.c_int32), ("serialize", C.c_int32), ("q_stream_overlap", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("windows", C.c_int64), ("levels", C.c_int64), ("swaps", C.c_int64),
+                ("swaps_by_type", C.c_int64 * 4), ("inner_windows", C.c_int64),
+                ("rejected_window", C.c_int64), ("rejected_row", C.c_int64),
+                ("rejected_n1", C.c_int32), ("rejected_n2", C.c_int32),
+                ("eq_flops", C.c_double), ("ms_schedule", C.c_double), ("ms_device", C.c_double),
+                ("ms_total", C.c_double), ("ms_h2d", C.c_double), ("ms_d2h", C.c_double)]
+
+    def to_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["swaps_by_type"] = list(self.swaps_by_type)
+        return d
+
+
+SN_OK, SN_ERR_REJECTED, SN_ERR_CUDA, SN_ERR_UNSUPPORTED = 0, 1, 2, 4
+
+EXPORTS = ["sn_default_opts", "sn_strerror", "sn_reorder_schur", "sn_reorder_schur_ex",
+           "sn_schedule_build", "sn_schedule_window_swaps", "sn_version"]
+
+_lib = None
+
+
+def lib():
+    """Load libsn_b200.so (fails loudly if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libsn_b200.so not built: run paper_1905_04975_b200.build() "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        i64, p = C.c_int64, C.c_void_p
+        L.sn_default_opts.argtypes = [C.POINTER(Opts)]
+        L.sn_strerror.argtypes = [C.c_int]
+        L.sn_strerror.restype = C.c_char_p
+        L.sn_version.restype = C.c_char_p
+        L.sn_reorder_schur.argtypes = [i64, p, i64, p, i64, p, C.POINTER(i64)]
+        L.sn_reorder_schur.restype = C.c_int
+        L.sn_reorder_schur_ex.argtypes = [C.POINTER(Opts), i64, p, i64, p, i64, p, C.POINTER(i64), p,
+                                          C.POINTER(Stats), p]
+        L.sn_reorder_schur_ex.restype = C.c_int
+        L.sn_schedule_build.argtypes = [i64, p, p, i64, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64),
+                                        p, p, p, p]
+        L.sn_schedule_build.restype = C.c_int
+        L.sn_schedule_window_swaps.argtypes = [i64, p, p, i64, i64, i64, i64, p, p, p]
+        L.sn_schedule_window_swaps.restype = i64
+        _lib = L
+    return _lib
+
+
+def default_opts(**kw) -> Opts:
+    o = Opts()
+    lib().sn_default_opts(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def strerror(code: int) -> str:
+    return lib().sn_strerror(code).decode()
+
+
+def _tensor_ptr(t):
+    if t is None:
+        return None, 0
+    import torch
+    assert t.dtype == torch.float64 and t.dim() == 2 and t.shape[0] == t.shape[1] and t.is_contiguous(), \
+        "expect a contiguous square fp64 tensor holding the transposed (column-major) matrix"
+    return C.c_void_p(t.data_ptr()), t.shape[0]
+
+
+def sn_reorder_schur(n, S, ldS, Q, ldQ, select, stream=None):
+    """The BASELINE signature sn_reorder_schur(n, S, ldS, Q, ldQ, select, &m) on raw pointers.
+
+    S, Q: integer addresses (device or host); select: np.int32 array (in/out).
+    Returns (rc, m)."""
+    m = C.c_int64()
+    sel = np.ascontiguousarray(select, np.int32)
+    rc = lib().sn_reorder_schur(n, C.c_void_p(S), ldS, None if Q is None else C.c_void_p(Q), ldQ,
+                                sel.ctypes.data_as(C.c_void_p), C.byref(m))
+    if isinstance(select, np.ndarray) and select.dtype == np.int32 and select.flags.c_contiguous:
+        select[:] = sel
+    return rc, m.value
+
+
+def reorder(S, Q, select, window: int = 256, stream=None, **opts):
+    """Reorder in place.  S, Q: torch fp64 tensors (column-major memory, see module doc), Q
+    may be None.  select: per-row int32 mask (copied).  Returns dict(rc, m, select, bmap,
+    stats)."""
+    import torch
+    ps, n = _tensor_ptr(S)
+    pq, nq = _tensor_ptr(Q)
+    if Q is not None:
+        assert nq == n and Q.device == S.device
+    o = default_opts(window=window, **opts)
+    sel = np.ascontiguousarray(select, np.int32).copy()
+    bmap = np.zeros(n, np.int8)
+    m = C.c_int64()
+    st = Stats()
+    if stream is None and S.is_cuda:
+        stream = torch.cuda.current_stream(S.device).cuda_stream
+    rc = lib().sn_reorder_schur_ex(C.byref(o), n, ps, n, pq, n, sel.ctypes.data_as(C.c_void_p), C.byref(m),
+                                   bmap.ctypes.data_as(C.c_void_p), C.byref(st),
+                                   None if stream is None else C.c_void_p(stream))
+    return {"rc": rc, "m": m.value, "select": sel, "bmap": bmap, "stats": st.to_dict()}
+
+
+def schedule(bmap, selrow, w: int):
+    """Host-only: the windows the library executes (schedule order)."""
+    bmap = np.ascontiguousarray(bmap, np.int8)
+    selrow = np.ascontiguousarray(selrow, np.int8)
+    n = len(bmap)
+    nw, ns, nl = C.c_int64(), C.c_int64(), C.c_int64()
+    L = lib()
+    rc = L.sn_schedule_build(n, bmap.ctypes.data_as(C.c_void_p), selrow.ctypes.data_as(C.c_void_p), w,
+                             C.byref(nw), C.byref(ns), C.byref(nl), None, None, None, None)
+    if rc:
+        raise ValueError("sn_schedule_build rc=%d" % rc)
+    j1, k, lev, sw = (np.zeros(nw.value, np.int64) for _ in range(4))
+    L.sn_schedule_build(n, bmap.ctypes.data_as(C.c_void_p), selrow.ctypes.data_as(C.c_void_p), w,
+                        C.byref(nw), C.byref(ns), C.byref(nl), j1.ctypes.data_as(C.c_void_p),
+                        k.ctypes.data_as(C.c_void_p), lev.ctypes.data_as(C.c_void_p), sw.ctypes.data_as(C.c_void_p))
+    return {"j1": j1, "k": k, "level": lev, "nswap": sw, "nlevels": nl.value, "total_swaps": ns.value}
+
+
+def window_swaps(bmap, selrow, w: int, t: int, inner_window: int = 64):
+    bmap = np.ascontiguousarray(bmap, np.int8)
+    selrow = np.ascontiguousarray(selrow, np.int8)
+    n = len(bmap)
+    cap = w * w
+    sj = np.zeros(cap, np.int64); s1 = np.zeros(cap, np.int8); s2 = np.zeros(cap, np.int8)
+    cnt = lib().sn_schedule_window_swaps(n, bmap.ctypes.data_as(C.c_void_p), selrow.ctypes.data_as(C.c_void_p),
+                                         w, inner_window, t, cap, sj.ctypes.data_as(C.c_void_p),
+                                         s1.ctypes.data_as(C.c_void_p), s2.ctypes.data_as(C.c_void_p))
+    if cnt < 0:
+        raise ValueError("sn_schedule_window_swaps rc=%d" % cnt)
+    return sj[:cnt], s1[:cnt], s2[:cnt]

@@ -1,0 +1,489 @@
+// sn_abi.cu -- C ABI entry points and the level executor (product code).
+//
+// Execution: the plan's windows are grouped by DAG level.  For each level:
+//   stream A:  window kernel (all windows of the level, one CTA each)  -> event W(s)
+//              left-update kernel (row panels right of every window)
+//              right-update kernel (column panels above every window)
+//   stream B:  waits W(s); Q-update kernel (columns of Q of every window)  -> event Q(s)
+// Windows of one level have disjoint diagonal ranges; the only conflicts inside a
+// level are between a left update of an upper window and a right update of a lower window
+// on the same off-diagonal rectangle; they commute mathematically and are serialised by
+// stream order (left, then right).  The next level's window kernel follows the right update
+// on stream A; the Q update of level s overlaps it on stream B.  Z slots are reused every
+// kZgen levels after the Q update that read them has finished.  This replaces the paper's
+// StarPU runtime with a static schedule known before the first launch.
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "sn_device.cuh"
+#include "sn_plan.h"
+#include "sn_reorder.h"
+
+namespace sn {
+namespace {
+
+constexpr int kZgen = 4;   // Z slot generations (levels in flight on stream B)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+};
+
+struct Workspace {
+  DevBuf wins, pool, prefix, status, ctl, Z, sub, bad;
+  cudaStream_t sB = nullptr;
+  cudaEvent_t evW[kZgen] = {}, evQ[kZgen] = {}, ev0 = nullptr, ev1 = nullptr, evJoin = nullptr;
+  int device = -1;
+};
+
+Workspace g_ws;
+std::mutex g_mu;
+
+double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+#define CK(x)                                                          \
+  do {                                                                 \
+    cudaError_t e_ = (x);                                              \
+    if (e_ != cudaSuccess) {                                           \
+      if (std::getenv("SN_DEBUG"))                                     \
+        std::fprintf(stderr, "sn: %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return SN_ERR_CUDA;                                              \
+    }                                                                  \
+  } while (0)
+
+int ensure_runtime(Workspace& ws) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (ws.device != dev) {
+    if (ws.sB) {
+      cudaStreamDestroy(ws.sB);
+      for (int i = 0; i < kZgen; ++i) { cudaEventDestroy(ws.evW[i]); cudaEventDestroy(ws.evQ[i]); }
+      cudaEventDestroy(ws.ev0); cudaEventDestroy(ws.ev1); cudaEventDestroy(ws.evJoin);
+    }
+    CK(cudaStreamCreateWithFlags(&ws.sB, cudaStreamNonBlocking));
+    for (int i = 0; i < kZgen; ++i) {
+      CK(cudaEventCreateWithFlags(&ws.evW[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ws.evQ[i], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreate(&ws.ev0));
+    CK(cudaEventCreate(&ws.ev1));
+    CK(cudaEventCreateWithFlags(&ws.evJoin, cudaEventDisableTiming));
+    ws.device = dev;
+  }
+  return 0;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// movers-first stable partition of a block range
+void partition(std::vector<uint8_t>& sz, std::vector<uint8_t>& sel, int64_t top, int64_t nb,
+               const uint8_t* psz, const uint8_t* psel) {
+  int64_t o = top;
+  for (int64_t b = 0; b < nb; ++b)
+    if (psel[b]) { sz[o] = psz[b]; sel[o] = 1; ++o; }
+  for (int64_t b = 0; b < nb; ++b)
+    if (!psel[b]) { sz[o] = psz[b]; sel[o] = 0; ++o; }
+}
+
+int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ, int32_t* select,
+        int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA) {
+  Workspace& ws = g_ws;
+  const double t_start = now_ms();
+  if (int rc = ensure_runtime(ws)) return rc;
+
+  // ---- a1: structure scan on the device, block map and selection on the host
+  CK(ws.sub.ensure((size_t)n + 8));
+  CK(ws.bad.ensure(8));
+  CK(cudaMemsetAsync(ws.bad.p, 0, 4, sA));
+  launch_scan(S, ldS, n, o.validate_lower, (uint8_t*)ws.sub.p, (int32_t*)ws.bad.p, sA);
+  CK(cudaGetLastError());
+  std::vector<uint8_t> sub((size_t)n);
+  int32_t bad = 0;
+  CK(cudaMemcpyAsync(sub.data(), ws.sub.p, (size_t)n, cudaMemcpyDeviceToHost, sA));
+  CK(cudaMemcpyAsync(&bad, ws.bad.p, 4, cudaMemcpyDeviceToHost, sA));
+  CK(cudaStreamSynchronize(sA));
+  if (bad) return -2;
+  std::vector<int8_t> bmap((size_t)n), selrow((size_t)n);
+  int64_t msel = 0;
+  for (int64_t i = 0; i < n;) {
+    if (sub[i]) {
+      if (i + 2 < n && sub[i + 1]) return -2;   // two consecutive nonzero subdiagonal entries
+      bmap[i] = 1; bmap[i + 1] = 2;
+      const int8_t s = (select[i] != 0 || select[i + 1] != 0) ? 1 : 0;
+      selrow[i] = selrow[i + 1] = s;
+      msel += 2 * s;
+      i += 2;
+    } else {
+      bmap[i] = 0;
+      selrow[i] = select[i] != 0 ? 1 : 0;
+      msel += selrow[i];
+      i += 1;
+    }
+  }
+  *m = msel;
+
+  // ---- a2: plan (window schedule, inner schedules, DAG levels)
+  Plan P;
+  int prc = build_plan(n, bmap.data(), selrow.data(), o.window, o.inner_window, o.max_windows, &P);
+  if (prc) return SN_ERR_UNSUPPORTED;
+  const int64_t nw = (int64_t)P.wins.size();
+  std::vector<int64_t> sorted(nw);
+  for (int64_t i = 0; i < nw; ++i) sorted[i] = i;
+  std::stable_sort(sorted.begin(), sorted.end(),
+                   [&](int64_t x, int64_t y) { return P.wins[x].level < P.wins[y].level; });
+  std::vector<int64_t> lstart(P.nlevels + 1, 0);
+  for (int64_t i = 0; i < nw; ++i) lstart[P.wins[sorted[i]].level + 1]++;
+  for (int64_t l = 0; l < P.nlevels; ++l) lstart[l + 1] += lstart[l];
+  int64_t maxper = 0;
+  for (int64_t l = 0; l < P.nlevels; ++l) maxper = std::max(maxper, lstart[l + 1] - lstart[l]);
+  const int NT = 64;
+  std::vector<WinDev> wd(nw);
+  std::vector<int32_t> pref;           // per level: 3 prefix arrays of (count+1)
+  std::vector<int64_t> pref_off(P.nlevels * 3);
+  std::vector<int32_t> nstrips(P.nlevels * 3);
+  double eq = 0.0;
+  for (int64_t l = 0; l < P.nlevels; ++l) {
+    const int64_t a = lstart[l], b = lstart[l + 1];
+    for (int kind = 0; kind < 3; ++kind) {
+      pref_off[l * 3 + kind] = (int64_t)pref.size();
+      int32_t acc = 0;
+      pref.push_back(0);
+      for (int64_t i = a; i < b; ++i) {
+        const WindowPlan& w = P.wins[sorted[i]];
+        int64_t cnt = 0;
+        if (kind == 0) cnt = (n - (w.j1 + w.k) + NT - 1) / NT;
+        else if (kind == 1) cnt = (w.j1 + NT - 1) / NT;
+        else cnt = Q ? (n + NT - 1) / NT : 0;
+        acc += (int32_t)cnt;
+        pref.push_back(acc);
+      }
+      nstrips[l * 3 + kind] = acc;
+    }
+    for (int64_t i = a; i < b; ++i) {
+      const WindowPlan& w = P.wins[sorted[i]];
+      WinDev& d = wd[i];
+      d.j1 = w.j1; d.k = w.k; d.nblk = w.nblk; d.ninner = w.ninner;
+      d.slot = (int32_t)((l % kZgen) * maxper + (i - a));
+      d.pool = w.pool; d.order = w.order;
+    }
+  }
+  const double t_plan = now_ms();
+
+  if (nw == 0) {
+    if (bmap_out) std::memcpy(bmap_out, bmap.data(), (size_t)n);
+    if (st) {
+      std::memset(st, 0, sizeof(*st));
+      st->rejected_window = -1; st->rejected_row = -1;
+      st->ms_schedule = t_plan - t_start;
+      st->ms_total = now_ms() - t_start;
+    }
+    // selection output: achieved mask = input mask normalised per block
+    for (int64_t i = 0; i < n; ++i) select[i] = selrow[i];
+    return 0;
+  }
+
+  // ---- uploads
+  CK(ws.wins.ensure(sizeof(WinDev) * nw));
+  CK(ws.pool.ensure(P.pool.size() + 8));
+  CK(ws.prefix.ensure(sizeof(int32_t) * pref.size()));
+  CK(ws.status.ensure(sizeof(int32_t) * nw));
+  CK(ws.ctl.ensure(sizeof(Control)));
+  CK(ws.Z.ensure(sizeof(double) * (size_t)kZslot * (size_t)(kZgen * maxper)));
+  CK(cudaMemcpyAsync(ws.wins.p, wd.data(), sizeof(WinDev) * nw, cudaMemcpyHostToDevice, sA));
+  CK(cudaMemcpyAsync(ws.pool.p, P.pool.data(), P.pool.size(), cudaMemcpyHostToDevice, sA));
+  CK(cudaMemcpyAsync(ws.prefix.p, pref.data(), sizeof(int32_t) * pref.size(), cudaMemcpyHostToDevice, sA));
+  CK(cudaMemsetAsync(ws.status.p, 0, sizeof(int32_t) * nw, sA));
+  CK(cudaMemsetAsync(ws.ctl.p, 0, sizeof(Control), sA));
+
+  const int mt = o.window <= 64 ? 64 : (o.window <= 128 ? 128 : 256);
+  WinDev* dw = (WinDev*)ws.wins.p;
+  int32_t* dstatus = (int32_t*)ws.status.p;
+  int32_t* dpref = (int32_t*)ws.prefix.p;
+  Control* dctl = (Control*)ws.ctl.p;
+  double* dZ = (double*)ws.Z.p;
+  const bool overlapQ = o.q_stream_overlap != 0 && Q != nullptr;
+  cudaStream_t sQ = overlapQ ? ws.sB : sA;
+
+  CK(cudaEventRecord(ws.ev0, sA));
+  if (overlapQ) {
+    CK(cudaStreamWaitEvent(ws.sB, ws.ev0, 0));
+  }
+  for (int64_t l = 0; l < P.nlevels; ++l) {
+    const int64_t a = lstart[l], cnt = lstart[l + 1] - a;
+    const int gen = (int)(l % kZgen);
+    if (overlapQ && l >= kZgen) CK(cudaStreamWaitEvent(sA, ws.evQ[gen], 0));
+    WindowArgs wa;
+    wa.wins = dw + a; wa.nwin = (int32_t)cnt; wa.base = (int32_t)a;
+    wa.pool = (const uint8_t*)ws.pool.p; wa.S = S; wa.ldS = ldS; wa.Z = dZ;
+    wa.status = dstatus; wa.ctl = dctl;
+    wa.force_order = o.force_reject_window; wa.force_swap = (int32_t)o.force_reject_swap;
+    launch_window(wa, sA);
+    CK(cudaGetLastError());
+    if (overlapQ) CK(cudaEventRecord(ws.evW[gen], sA));
+    PanelArgs pa;
+    pa.wins = dw + a; pa.nwin = (int32_t)cnt; pa.base = (int32_t)a; pa.status = dstatus;
+    pa.n = n; pa.Z = dZ;
+    pa.M = S; pa.ld = ldS;
+    pa.prefix = dpref + pref_off[l * 3 + 0];
+    launch_panel(0, mt, pa, nstrips[l * 3 + 0], sA);
+    pa.prefix = dpref + pref_off[l * 3 + 1];
+    launch_panel(1, mt, pa, nstrips[l * 3 + 1], sA);
+    CK(cudaGetLastError());
+    if (Q) {
+      if (overlapQ) CK(cudaStreamWaitEvent(sQ, ws.evW[gen], 0));
+      pa.M = Q; pa.ld = ldQ;
+      pa.prefix = dpref + pref_off[l * 3 + 2];
+      launch_panel(2, mt, pa, nstrips[l * 3 + 2], sQ);
+      CK(cudaGetLastError());
+      if (overlapQ) CK(cudaEventRecord(ws.evQ[gen], sQ));
+    }
+    if (o.serialize) {
+      CK(cudaStreamSynchronize(sA));
+      if (overlapQ) CK(cudaStreamSynchronize(sQ));
+    }
+  }
+  if (overlapQ) {
+    CK(cudaEventRecord(ws.evJoin, sQ));
+    CK(cudaStreamWaitEvent(sA, ws.evJoin, 0));
+  }
+  CK(cudaEventRecord(ws.ev1, sA));
+  Control ctl;
+  CK(cudaMemcpyAsync(&ctl, dctl, sizeof(Control), cudaMemcpyDeviceToHost, sA));
+  CK(cudaStreamSynchronize(sA));
+  float dev_ms = 0.f;
+  CK(cudaEventElapsedTime(&dev_ms, ws.ev0, ws.ev1));
+
+  // ---- outputs: final block list
+  std::vector<uint8_t> fsz, fsel;
+  std::vector<int32_t> status;
+  int64_t executed = nw, swaps = 0;
+  double eqf = 0.0;
+  int64_t sbt[4] = {0, 0, 0, 0};
+  if (!ctl.abort) {
+    fsz = P.final_sz; fsel = P.final_sel;
+    for (const auto& w : P.wins) {
+      swaps += w.nswap;
+      for (int q = 0; q < 4; ++q) sbt[q] += w.swaps_by_type[q];
+    }
+  } else {
+    status.resize(nw);
+    CK(cudaMemcpy(status.data(), dstatus, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n;) {
+      const int s = bmap[i] == 1 ? 2 : 1;
+      fsz.push_back((uint8_t)s); fsel.push_back((uint8_t)selrow[i]);
+      i += s;
+    }
+    std::vector<int64_t> pos_of(nw);
+    for (int64_t i = 0; i < nw; ++i) pos_of[sorted[i]] = i;
+    executed = 0;
+    for (int64_t t = 0; t < nw; ++t) {
+      const WindowPlan& w = P.wins[t];
+      const int32_t stt = status[pos_of[t]];
+      if (stt == kWinDone) {
+        partition(fsz, fsel, w.top, w.nblk, P.pool.data() + w.pool, P.pool.data() + w.pool + w.nblk);
+        swaps += w.nswap;
+        for (int q = 0; q < 4; ++q) sbt[q] += w.swaps_by_type[q];
+        ++executed;
+      } else if (stt == kWinPartial) {
+        std::memcpy(fsz.data() + w.top, ctl.rej_sz, (size_t)w.nblk);
+        std::memcpy(fsel.data() + w.top, ctl.rej_sel, (size_t)w.nblk);
+        swaps += ctl.rej_swaps_done;
+        ++executed;
+      }
+    }
+  }
+  for (int64_t i = 0; i < nw; ++i) {
+    const WindowPlan& w = P.wins[sorted[i]];
+    if (ctl.abort && status[i] == kWinSkipped) continue;
+    const double k2 = 2.0 * (double)w.k * (double)w.k;
+    eqf += k2 * ((double)(n - w.j1 - w.k) + (double)w.j1 + (Q ? (double)n : 0.0));
+  }
+  (void)eq;
+  {
+    int64_t r = 0;
+    for (size_t b = 0; b < fsz.size(); ++b) {
+      for (int q = 0; q < fsz[b]; ++q) {
+        select[r + q] = fsel[b];
+        if (bmap_out) bmap_out[r + q] = (int8_t)(fsz[b] == 1 ? 0 : 1 + q);
+      }
+      r += fsz[b];
+    }
+  }
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->windows = executed;
+    st->levels = P.nlevels;
+    st->swaps = swaps;
+    for (int q = 0; q < 4; ++q) st->swaps_by_type[q] = sbt[q];
+    st->inner_windows = P.ninner;
+    st->rejected_window = -1;
+    st->rejected_row = -1;
+    if (ctl.abort) {
+      st->rejected_window = P.wins[sorted[ctl.rej_window]].order;
+      st->rejected_row = ctl.rej_row;
+      st->rejected_n1 = ctl.rej_n1;
+      st->rejected_n2 = ctl.rej_n2;
+    }
+    st->eq_flops = eqf;
+    st->ms_schedule = t_plan - t_start;
+    st->ms_device = dev_ms;
+    st->ms_total = now_ms() - t_start;
+  }
+  return ctl.abort ? SN_ERR_REJECTED : SN_OK;
+}
+
+}  // namespace
+}  // namespace sn
+
+extern "C" {
+
+void sn_default_opts(sn_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->window = 256;
+  o->inner_window = 64;
+  o->max_windows = -1;
+  o->force_reject_window = -1;
+  o->force_reject_swap = -1;
+  o->validate_lower = 0;
+  o->serialize = 0;
+  o->q_stream_overlap = 1;
+}
+
+const char* sn_strerror(int code) {
+  switch (code) {
+    case SN_OK: return "success";
+    case SN_ERR_REJECTED: return "a block swap was rejected by the stability test; S and Q hold a valid, partially reordered Schur form";
+    case SN_ERR_CUDA: return "CUDA error (no usable device, out of memory, or a kernel failure)";
+    case SN_ERR_UNSUPPORTED: return "unsupported option value";
+    default: break;
+  }
+  if (code < 0) return "invalid argument (-i: argument i of sn_reorder_schur)";
+  return "unknown error";
+}
+
+const char* sn_version(void) { return "sn_b200 0.1 (sm_100a)"; }
+
+int sn_reorder_schur_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ,
+                        int32_t* select, int64_t* m, int8_t* bmap_out, sn_stats* stats, void* stream) {
+  sn_opts o;
+  if (opts) o = *opts; else sn_default_opts(&o);
+  if (m == nullptr) return -7;
+  *m = 0;
+  if (n < 0) return -1;
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->rejected_window = -1;
+    stats->rejected_row = -1;
+  }
+  if (n == 0) return 0;
+  if (S == nullptr) return -2;
+  if (ldS < n) return -3;
+  if (Q != nullptr && ldQ < n) return -5;
+  if (select == nullptr) return -6;
+  if (o.window < 4 || o.window > 256 || o.inner_window < 4 || o.inner_window > 64) return SN_ERR_UNSUPPORTED;
+  std::lock_guard<std::mutex> lock(sn::g_mu);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return SN_ERR_CUDA;
+  }
+  cudaStream_t sA = (cudaStream_t)stream;
+  const bool devS = sn::is_device_ptr(S);
+  const bool devQ = Q == nullptr || sn::is_device_ptr(Q);
+  if (devS != devQ) return -4;
+  if (devS) return sn::run(o, n, S, ldS, Q, ldQ, select, m, bmap_out, stats, sA);
+  // host buffers: stage through device memory (the copies are part of the call)
+  const double t0 = sn::now_ms();
+  double *dS = nullptr, *dQ = nullptr;
+  const size_t bytes = sizeof(double) * (size_t)n * (size_t)n;
+  if (cudaMalloc(&dS, bytes) != cudaSuccess) return SN_ERR_CUDA;
+  if (Q && cudaMalloc(&dQ, bytes) != cudaSuccess) { cudaFree(dS); return SN_ERR_CUDA; }
+  int rc = SN_OK;
+  if (cudaMemcpy2DAsync(dS, n * 8, S, ldS * 8, n * 8, n, cudaMemcpyHostToDevice, sA) != cudaSuccess ||
+      (Q && cudaMemcpy2DAsync(dQ, n * 8, Q, ldQ * 8, n * 8, n, cudaMemcpyHostToDevice, sA) != cudaSuccess) ||
+      cudaStreamSynchronize(sA) != cudaSuccess)
+    rc = SN_ERR_CUDA;
+  const double t1 = sn::now_ms();
+  if (rc == SN_OK) rc = sn::run(o, n, dS, n, dQ, n, select, m, bmap_out, stats, sA);
+  const double t2 = sn::now_ms();
+  if (rc == SN_OK || rc == SN_ERR_REJECTED) {
+    if (cudaMemcpy2DAsync(S, ldS * 8, dS, n * 8, n * 8, n, cudaMemcpyDeviceToHost, sA) != cudaSuccess ||
+        (Q && cudaMemcpy2DAsync(Q, ldQ * 8, dQ, n * 8, n * 8, n, cudaMemcpyDeviceToHost, sA) != cudaSuccess) ||
+        cudaStreamSynchronize(sA) != cudaSuccess)
+      rc = SN_ERR_CUDA;
+  }
+  const double t3 = sn::now_ms();
+  cudaFree(dS);
+  if (dQ) cudaFree(dQ);
+  if (stats) {
+    stats->ms_h2d = t1 - t0;
+    stats->ms_d2h = t3 - t2;
+    stats->ms_total = t3 - t0;
+  }
+  return rc;
+}
+
+int sn_reorder_schur(int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ, int32_t* select, int64_t* m) {
+  return sn_reorder_schur_ex(nullptr, n, S, ldS, Q, ldQ, select, m, nullptr, nullptr, nullptr);
+}
+
+int sn_schedule_build(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w, int64_t* nwin,
+                      int64_t* nswap, int64_t* nlevels, int64_t* win_j1, int64_t* win_k, int64_t* win_level,
+                      int64_t* win_nswap) {
+  if (n < 0) return -1;
+  if (n > 0 && (!bmap || !selrow)) return -2;
+  if (!nwin || !nswap || !nlevels) return -5;
+  sn::Plan P;
+  int rc = sn::build_plan(n, bmap, selrow, w, 64, -1, &P);
+  if (rc) return rc;
+  *nwin = (int64_t)P.wins.size();
+  *nswap = P.nswap;
+  *nlevels = P.nlevels;
+  if (win_j1) {
+    for (size_t t = 0; t < P.wins.size(); ++t) {
+      win_j1[t] = P.wins[t].j1;
+      if (win_k) win_k[t] = P.wins[t].k;
+      if (win_level) win_level[t] = P.wins[t].level;
+      if (win_nswap) win_nswap[t] = P.wins[t].nswap;
+    }
+  }
+  return 0;
+}
+
+int64_t sn_schedule_window_swaps(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w,
+                                 int64_t inner_window, int64_t t, int64_t cap, int64_t* swap_j, int8_t* swap_n1,
+                                 int8_t* swap_n2) {
+  sn::Plan P;
+  int rc = sn::build_plan(n, bmap, selrow, w, inner_window, t + 1, &P);
+  if (rc) return rc;
+  return sn::window_swaps(P, t, cap, swap_j, swap_n1, swap_n2);
+}
+
+}  // extern "C"

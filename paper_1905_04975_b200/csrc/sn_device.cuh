@@ -1,0 +1,73 @@
+// sn_device.cuh -- device-side data layout shared by the executor and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sn {
+
+constexpr int kZld = 256;                 // Z slots are 256 x 256, column-major, ld 256
+constexpr int64_t kZslot = (int64_t)kZld * kZld;
+constexpr int kInner = 64;                // max rows of an in-kernel inner window
+
+// One window, as seen by the kernels (sorted by level).
+struct WinDev {
+  int64_t j1;        // first row of the window
+  int32_t k;         // rows
+  int32_t nblk;      // blocks
+  int32_t ninner;    // inner windows
+  int32_t slot;      // Z slot
+  int64_t pool;      // byte offset of sz[nblk], sel[nblk], (pad), inner[2*ninner] (uint16)
+  int64_t order;     // schedule order
+};
+
+// Per-call device control block.
+struct Control {
+  int32_t abort;            // set by a window kernel that rejected a swap
+  int32_t rej_window;       // sorted index of the rejecting window
+  int32_t rej_swaps_done;   // swaps completed in that window before the rejected one
+  int32_t rej_row;          // global first row of the rejected swap
+  int32_t rej_n1, rej_n2;
+  int32_t pad[2];
+  uint8_t rej_sz[256];      // block list of the rejecting window after its last good swap
+  uint8_t rej_sel[256];
+};
+
+// status[] of a window: 0 not executed, 1 complete, 2 partial (rejected inside; Z valid)
+enum : int32_t { kWinSkipped = 0, kWinDone = 1, kWinPartial = 2 };
+
+struct WindowArgs {
+  const WinDev* wins;       // this level's windows
+  int32_t nwin;
+  int32_t base;             // sorted index of wins[0]
+  const uint8_t* pool;
+  double* S;
+  int64_t ldS;
+  double* Z;                // slot array base
+  int32_t* status;          // indexed by sorted index
+  Control* ctl;
+  int64_t force_order;      // debug: schedule order of the window to reject in (-1 none)
+  int32_t force_swap;       // debug: swap index (execution order) to reject
+};
+
+struct PanelArgs {
+  const WinDev* wins;       // this level's windows
+  int32_t nwin;
+  int32_t base;
+  const int32_t* prefix;    // nwin+1 cumulative strip counts of this kind
+  const int32_t* status;
+  double* M;                // S (left/right) or Q
+  int64_t ld;
+  int64_t n;
+  const double* Z;
+};
+
+// kernel launchers (sn_kernels_*.cu)
+void launch_scan(const double* S, int64_t ldS, int64_t n, int32_t validate_lower, uint8_t* subflag,
+                 int32_t* bad, cudaStream_t st);
+void launch_window(const WindowArgs& a, cudaStream_t st);
+size_t window_smem_bytes();
+// kind: 0 = left update of S, 1 = right update of S, 2 = Q update; mt = 64/128/256
+void launch_panel(int kind, int mt, const PanelArgs& a, int32_t nstrips, cudaStream_t st);
+int panel_strip_width(int kind, int mt);
+
+}  // namespace sn

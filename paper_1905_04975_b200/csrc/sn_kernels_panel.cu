@@ -1,0 +1,225 @@
+// sn_kernels_panel.cu -- the right/left update tasks ("applies
+// accumulated right-hand [left-hand] side updates using level-3 BLAS operations") and the
+// Q update (Q <- Q*Q3), as in-place FP64 tensor-core GEMMs on sm_100a.
+//
+//   left  (kind 0):  S[j1:j2, c0:c0+NT]  <- Z^T * S[j1:j2, c0:c0+NT]     (row panel right)
+//   right (kind 1):  S[r0:r0+NT, j1:j2]  <- S[r0:r0+NT, j1:j2] * Z       (column panel above)
+//   Q     (kind 2):  Q[r0:r0+NT, j1:j2]  <- Q[r0:r0+NT, j1:j2] * Z
+//
+// One CTA owns one strip for the whole K = k extent, so the strip can be overwritten in
+// place after its last K chunk is consumed (no other CTA touches it).  All three kinds are
+// the same product  C[m][x] = sum_kk Z[kk][m] * B[kk][x]  with A = Z^T from the Z slot and B
+// the strip (x = column for left, row for right/Q).  Operands are staged through shared
+// memory with a 3-stage cp.async pipeline and multiplied with mma.sync.m16n8k8.f64 (DMMA),
+// the FP64 tensor-core path of sm_100 (tcgen05 has no f64 kind).  DESIGN.md §6.
+#include <cstdint>
+
+#include "sn_device.cuh"
+
+namespace sn {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int KC = 16;        // K chunk
+constexpr int LDA = KC + 4;   // As[m][kk], row stride == 4 mod 16 (conflict-free fragments)
+constexpr int NSTAGE = 3;
+
+__device__ __forceinline__ void mma_16x8x8(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+template <int MT, int NT, int KIND>
+struct Cfg {
+  static constexpr bool LEFT = (KIND == 0);
+  static constexpr int WM = 4, WN = 2;
+  static constexpr int MI = MT / (WM * 16);   // m16 tiles per warp
+  static constexpr int NI = NT / (WN * 8);    // n8 tiles per warp
+  static constexpr int LDB = LEFT ? (KC + 4) : (NT + 4);   // Bs[x][kk] (left) or Bs[kk][x]
+  static constexpr int A_ELEMS = MT * LDA;
+  static constexpr int B_ELEMS = LEFT ? NT * LDB : KC * LDB;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM = sizeof(double) * (size_t)STAGE * NSTAGE;
+};
+
+template <int MT, int NT, int KIND>
+__global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
+  using C = Cfg<MT, NT, KIND>;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  // strip -> (window, index) by binary search over the level's prefix
+  const int sid = blockIdx.x;
+  int lo = 0, hi = a.nwin - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.prefix[mid] <= sid) lo = mid; else hi = mid - 1;
+  }
+  const int w = lo;
+  if (a.status[a.base + w] == kWinSkipped) return;
+  const WinDev wd = a.wins[w];
+  const int strip = sid - a.prefix[w];
+  const int k = wd.k;
+  const int64_t j1 = wd.j1, ld = a.ld;
+  double* M = a.M;
+  const double* Z = a.Z + (int64_t)wd.slot * kZslot;
+  int64_t x0;      // first column (left) or row (right/Q) of the strip
+  int nx;          // valid columns/rows
+  if (C::LEFT) {
+    x0 = j1 + k + (int64_t)strip * NT;
+    nx = (int)min((int64_t)NT, a.n - x0);
+  } else {
+    x0 = (int64_t)strip * NT;
+    const int64_t lim = (KIND == 1) ? j1 : a.n;
+    nx = (int)min((int64_t)NT, lim - x0);
+  }
+  const int nk = (k + KC - 1) / KC;
+
+  auto load_stage = [&](int stage, int kc) {
+    double* As = smem + stage * C::STAGE;
+    double* Bs = As + C::A_ELEMS;
+    const int kk0 = kc * KC;
+    // A = Z^T chunk: As[m][kk] = Z[kk0 + kk + m*256]; 16-byte copies, 8 per row
+    for (int idx = tid; idx < MT * (KC / 2); idx += kThreads) {
+      const int m = idx / (KC / 2), part = idx % (KC / 2);
+      cp_async16(As + m * LDA + part * 2, Z + (int64_t)m * kZld + kk0 + part * 2);
+    }
+    if (C::LEFT) {
+      // Bs[c][kk] = M[(j1 + kk0 + kk) + (x0 + c)*ld]
+      for (int idx = tid; idx < NT * KC; idx += kThreads) {
+        const int c = idx / KC, kk = idx % KC;
+        const bool v = (c < nx) && (kk0 + kk < k);
+        const double* src = v ? M + (j1 + kk0 + kk) + (x0 + c) * ld : M;
+        cp_async8(Bs + c * C::LDB + kk, src, v);
+      }
+    } else {
+      // Bs[kk][r] = M[(x0 + r) + (j1 + kk0 + kk)*ld]
+      for (int idx = tid; idx < NT * KC; idx += kThreads) {
+        const int kk = idx / NT, r = idx % NT;
+        const bool v = (r < nx) && (kk0 + kk < k);
+        const double* src = v ? M + (x0 + r) + (j1 + kk0 + kk) * ld : M;
+        cp_async8(Bs + kk * C::LDB + r, src, v);
+      }
+    }
+  };
+
+  double acc[C::MI][C::NI][4];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
+
+  const int wm0 = (warp % C::WM) * (MT / C::WM);
+  const int wn0 = (warp / C::WM) * (NT / C::WN);
+
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_wait<NSTAGE - 2>();
+    __syncthreads();
+    // prefetch chunk kc + NSTAGE - 1 into the stage freed by chunk kc - 1
+    if (kc + NSTAGE - 1 < nk) load_stage((kc + NSTAGE - 1) % NSTAGE, kc + NSTAGE - 1);
+    cp_commit();
+    const double* As = smem + (kc % NSTAGE) * C::STAGE;
+    const double* Bs = As + C::A_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < KC; ks += 8) {
+      double af[C::MI][4], bf[C::NI][2];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) {
+        const double* ap = As + (wm0 + i * 16 + g) * LDA + ks + t;
+        af[i][0] = ap[0];
+        af[i][1] = ap[8 * LDA];
+        af[i][2] = ap[4];
+        af[i][3] = ap[8 * LDA + 4];
+      }
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        const int xx = wn0 + j * 8 + g;
+        if (C::LEFT) {
+          bf[j][0] = Bs[xx * C::LDB + ks + t];
+          bf[j][1] = Bs[xx * C::LDB + ks + t + 4];
+        } else {
+          bf[j][0] = Bs[(ks + t) * C::LDB + xx];
+          bf[j][1] = Bs[(ks + t + 4) * C::LDB + xx];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) mma_16x8x8(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_wait<0>();
+  // every K chunk of this strip has been read by this CTA: overwrite in place
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = wm0 + i * 16 + g + 8 * h;
+        if (m >= k) continue;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int xx = wn0 + j * 8 + 2 * t + q;
+          if (xx >= nx) continue;
+          const double v = acc[i][j][2 * h + q];
+          if (C::LEFT) M[(j1 + m) + (x0 + xx) * ld] = v;
+          else M[(x0 + xx) + (j1 + m) * ld] = v;
+        }
+      }
+}
+
+template <int MT, int NT, int KIND>
+void launch_t(const PanelArgs& a, int32_t nstrips, cudaStream_t st) {
+  using C = Cfg<MT, NT, KIND>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(panel_kernel<MT, NT, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    attr = true;
+  }
+  panel_kernel<MT, NT, KIND><<<nstrips, kThreads, C::SMEM, st>>>(a);
+}
+
+template <int KIND>
+void launch_kind(int mt, const PanelArgs& a, int32_t nstrips, cudaStream_t st) {
+  if (mt <= 64) launch_t<64, 64, KIND>(a, nstrips, st);
+  else if (mt <= 128) launch_t<128, 64, KIND>(a, nstrips, st);
+  else launch_t<256, 64, KIND>(a, nstrips, st);
+}
+
+}  // namespace
+
+int panel_strip_width(int kind, int mt) { (void)kind; (void)mt; return 64; }
+
+void launch_panel(int kind, int mt, const PanelArgs& a, int32_t nstrips, cudaStream_t st) {
+  if (nstrips <= 0) return;
+  if (kind == 0) launch_kind<0>(mt, a, nstrips, st);
+  else if (kind == 1) launch_kind<1>(mt, a, nstrips, st);
+  else launch_kind<2>(mt, a, nstrips, st);
+}
+
+}  // namespace sn
