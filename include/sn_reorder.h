@@ -57,7 +57,8 @@ typedef struct sn_opts {
   int32_t serialize;         /* 1: debug, synchronise after every launch */
   int32_t q_stream_overlap;  /* 1 (default): Q updates on a second stream, overlapping the
                                 next level's window tasks */
-  int32_t reserved;
+  int32_t profile;           /* 1: bracket every kernel launch with CUDA events on its own
+                                stream and report per-kernel-kind times in sn_stats */
 } sn_opts;
 
 /* Statistics of one call. */
@@ -76,6 +77,11 @@ typedef struct sn_stats {
   double ms_device;          /* device time of the reordering (CUDA events) */
   double ms_total;           /* wall time of the call */
   double ms_h2d, ms_d2h;     /* host-pointer staging copies (0 for device pointers) */
+  /* per kernel kind: 0 window, 1 left update, 2 right update, 3 Q update, 4 scan */
+  int64_t launches[5];       /* kernel launches of this call */
+  double ms_kernel[5];       /* summed event time per kind (opts.profile = 1, else 0) */
+  double flops_kernel[5];    /* algorithmic flops per kind (updates: 2 k^2 x panel extent) */
+  double bytes_kernel[5];    /* algorithmic HBM bytes per kind (panel read + write once) */
 } sn_stats;
 
 void sn_default_opts(sn_opts* o);

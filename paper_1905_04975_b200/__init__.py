@@ -50,7 +50,7 @@ class Opts(C.Structure):
     _fields_ = [("window", C.c_int64), ("inner_window", C.c_int64), ("max_windows", C.c_int64),
                 ("force_reject_window", C.c_int64), ("force_reject_swap", C.c_int64),
                 ("validate_lower", C.c_int32), ("serialize", C.c_int32), ("q_stream_overlap", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("profile", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -59,11 +59,14 @@ class Stats(C.Structure):
                 ("rejected_window", C.c_int64), ("rejected_row", C.c_int64),
                 ("rejected_n1", C.c_int32), ("rejected_n2", C.c_int32),
                 ("eq_flops", C.c_double), ("ms_schedule", C.c_double), ("ms_device", C.c_double),
-                ("ms_total", C.c_double), ("ms_h2d", C.c_double), ("ms_d2h", C.c_double)]
+                ("ms_total", C.c_double), ("ms_h2d", C.c_double), ("ms_d2h", C.c_double),
+                ("launches", C.c_int64 * 5), ("ms_kernel", C.c_double * 5), ("flops_kernel", C.c_double * 5),
+                ("bytes_kernel", C.c_double * 5)]
 
     def to_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}
-        d["swaps_by_type"] = list(self.swaps_by_type)
+        for f in ("swaps_by_type", "launches", "ms_kernel", "flops_kernel", "bytes_kernel"):
+            d[f] = list(getattr(self, f))
         return d
 
 

@@ -47,6 +47,7 @@ struct DevBuf {
 
 struct Workspace {
   DevBuf wins, pool, prefix, status, ctl, Z, sub, bad;
+  std::vector<cudaEvent_t> prof;   // event pool for opts.profile
   cudaStream_t sB = nullptr;
   cudaEvent_t evW[kZgen] = {}, evQ[kZgen] = {}, ev0 = nullptr, ev1 = nullptr, evJoin = nullptr;
   int device = -1;
@@ -116,12 +117,36 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   Workspace& ws = g_ws;
   const double t_start = now_ms();
   if (int rc = ensure_runtime(ws)) return rc;
+  int64_t launches[5] = {0, 0, 0, 0, 0};
+  std::vector<std::pair<int, int>> prof_marks;   // (kind, first event index)
+  size_t prof_used = 0;
+  auto prof_begin = [&](int kind, cudaStream_t s) -> int {
+    if (!o.profile) return -1;
+    while (ws.prof.size() < prof_used + 2) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return -1;
+      ws.prof.push_back(e);
+    }
+    const int idx = (int)prof_used;
+    prof_used += 2;
+    cudaEventRecord(ws.prof[idx], s);
+    prof_marks.push_back({kind, idx});
+    return idx;
+  };
+  auto prof_end = [&](int idx, cudaStream_t s) {
+    if (idx >= 0) cudaEventRecord(ws.prof[idx + 1], s);
+  };
 
   // ---- a1: structure scan on the device, block map and selection on the host
   CK(ws.sub.ensure((size_t)n + 8));
   CK(ws.bad.ensure(8));
   CK(cudaMemsetAsync(ws.bad.p, 0, 4, sA));
-  launch_scan(S, ldS, n, o.validate_lower, (uint8_t*)ws.sub.p, (int32_t*)ws.bad.p, sA);
+  {
+    const int pe = prof_begin(4, sA);
+    launch_scan(S, ldS, n, o.validate_lower, (uint8_t*)ws.sub.p, (int32_t*)ws.bad.p, sA);
+    prof_end(pe, sA);
+    launches[4] += (o.validate_lower && n > 2) ? 2 : 1;
+  }
   CK(cudaGetLastError());
   std::vector<uint8_t> sub((size_t)n);
   int32_t bad = 0;
@@ -202,6 +227,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
       st->rejected_window = -1; st->rejected_row = -1;
       st->ms_schedule = t_plan - t_start;
       st->ms_total = now_ms() - t_start;
+      st->launches[4] = launches[4];
     }
     // selection output: achieved mask = input mask normalised per block
     for (int64_t i = 0; i < n; ++i) select[i] = selrow[i];
@@ -243,23 +269,33 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     wa.pool = (const uint8_t*)ws.pool.p; wa.S = S; wa.ldS = ldS; wa.Z = dZ;
     wa.status = dstatus; wa.ctl = dctl;
     wa.force_order = o.force_reject_window; wa.force_swap = (int32_t)o.force_reject_swap;
+    int pe = prof_begin(0, sA);
     launch_window(wa, sA);
+    prof_end(pe, sA);
+    launches[0]++;
     CK(cudaGetLastError());
     if (overlapQ) CK(cudaEventRecord(ws.evW[gen], sA));
     PanelArgs pa;
     pa.wins = dw + a; pa.nwin = (int32_t)cnt; pa.base = (int32_t)a; pa.status = dstatus;
     pa.n = n; pa.Z = dZ;
     pa.M = S; pa.ld = ldS;
-    pa.prefix = dpref + pref_off[l * 3 + 0];
-    launch_panel(0, mt, pa, nstrips[l * 3 + 0], sA);
-    pa.prefix = dpref + pref_off[l * 3 + 1];
-    launch_panel(1, mt, pa, nstrips[l * 3 + 1], sA);
+    for (int kind = 0; kind < 2; ++kind) {
+      if (nstrips[l * 3 + kind] <= 0) continue;
+      pa.prefix = dpref + pref_off[l * 3 + kind];
+      pe = prof_begin(1 + kind, sA);
+      launch_panel(kind, mt, pa, nstrips[l * 3 + kind], sA);
+      prof_end(pe, sA);
+      launches[1 + kind]++;
+    }
     CK(cudaGetLastError());
     if (Q) {
       if (overlapQ) CK(cudaStreamWaitEvent(sQ, ws.evW[gen], 0));
       pa.M = Q; pa.ld = ldQ;
       pa.prefix = dpref + pref_off[l * 3 + 2];
+      pe = prof_begin(3, sQ);
       launch_panel(2, mt, pa, nstrips[l * 3 + 2], sQ);
+      prof_end(pe, sQ);
+      launches[3]++;
       CK(cudaGetLastError());
       if (overlapQ) CK(cudaEventRecord(ws.evQ[gen], sQ));
     }
@@ -318,11 +354,22 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
       }
     }
   }
+  double fk[5] = {0, 0, 0, 0, 0}, bk[5] = {0, 0, 0, 0, 0};
   for (int64_t i = 0; i < nw; ++i) {
     const WindowPlan& w = P.wins[sorted[i]];
     if (ctl.abort && status[i] == kWinSkipped) continue;
-    const double k2 = 2.0 * (double)w.k * (double)w.k;
-    eqf += k2 * ((double)(n - w.j1 - w.k) + (double)w.j1 + (Q ? (double)n : 0.0));
+    const double kd = (double)w.k, k2 = 2.0 * kd * kd;
+    const double eL = (double)(n - w.j1 - w.k), eR = (double)w.j1, eQ = Q ? (double)n : 0.0;
+    eqf += k2 * (eL + eR + eQ);
+    fk[1] += k2 * eL; fk[2] += k2 * eR; fk[3] += k2 * eQ;
+    bk[1] += 16.0 * kd * eL; bk[2] += 16.0 * kd * eR; bk[3] += 16.0 * kd * eQ;
+    bk[0] += 16.0 * kd * kd + 8.0 * kZslot;
+  }
+  bk[4] = 8.0 * (double)n + (o.validate_lower ? 4.0 * (double)n * (double)n : 0.0);
+  double mk[5] = {0, 0, 0, 0, 0};
+  for (auto& pm : prof_marks) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ws.prof[pm.second], ws.prof[pm.second + 1]) == cudaSuccess) mk[pm.first] += ms;
   }
   (void)eq;
   {
@@ -354,6 +401,12 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     st->ms_schedule = t_plan - t_start;
     st->ms_device = dev_ms;
     st->ms_total = now_ms() - t_start;
+    for (int q = 0; q < 5; ++q) {
+      st->launches[q] = launches[q];
+      st->ms_kernel[q] = mk[q];
+      st->flops_kernel[q] = fk[q];
+      st->bytes_kernel[q] = bk[q];
+    }
   }
   return ctl.abort ? SN_ERR_REJECTED : SN_OK;
 }

@@ -1,0 +1,204 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, on the GPU (-m gpu).
+
+Bar (BASELINE.json north_star): block map and selection mask bit-exact; S and Q elementwise
+within 1e-9 * ||S||_F; the invariants of tests/helpers.check_reordering.  The GPU executes
+the swaps of a window in a different (commuting) order than the oracle (inner windows,
+DESIGN.md §4), so agreement is to rounding, far inside the bar; the measured maxima are
+printed.  Inputs come from workloads/ only; expected values only from oracle/.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1905_04975_b200 as sn
+from tests.helpers import EPS, bmap_from_S, blocks_of, check_reordering
+from workloads import make_config, make_problem
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    sn.build()
+    assert torch.cuda.is_available()
+
+
+def run_both(p, w=None, q=True, **opts):
+    w = w or p.w
+    S0 = p.S_np().copy(order="F")
+    Q0 = p.Q_np().copy(order="F") if (q and p.Q is not None) else None
+    ref = oracle.reorder(S0, Q0, p.select, w=w, mode=1)
+    S = p.S.cuda().contiguous()
+    Q = p.Q.cuda().contiguous() if Q0 is not None else None
+    got = sn.reorder(S, Q, p.select, window=w, validate_lower=1, **opts)
+    torch.cuda.synchronize()
+    return S0, Q0, ref, got, S.cpu().numpy().T, (Q.cpu().numpy().T if Q is not None else None)
+
+
+def assert_parity(S0, Q0, ref, got, Sg, Qg, label=""):
+    assert got["rc"] == 0 == ref["rc"]
+    assert got["m"] == ref["m"]
+    np.testing.assert_array_equal(got["bmap"], ref["bmap"])
+    np.testing.assert_array_equal(got["select"], ref["select"])
+    nS = np.linalg.norm(S0)
+    dS = np.abs(Sg - ref["S"]).max() if S0.size else 0.0
+    dQ = np.abs(Qg - ref["Q"]).max() if Qg is not None and Qg.size else 0.0
+    print("%s max|dS|/||S||=%.3g max|dQ|=%.3g windows=%d swaps=%d" % (
+        label, dS / max(nS, 1e-300), dQ, got["stats"]["windows"], got["stats"]["swaps"]))
+    assert dS <= TOL * nS and dQ <= TOL * nS
+    assert got["stats"]["windows"] == ref["stats"]["windows"]
+    assert got["stats"]["swaps"] == ref["stats"]["swaps"]
+    return dS / max(nS, 1e-300), dQ
+
+
+def test_config0_parity():
+    p = make_config(0, seed=1)
+    S0, Q0, ref, got, Sg, Qg = run_both(p)
+    assert_parity(S0, Q0, ref, got, Sg, Qg, "config0")
+    check_reordering(S0, Q0, p.select, Sg, Qg, got["select"], got["m"], got["bmap"])
+
+
+@pytest.mark.parametrize("n,p2,w,psel,q,seed", [
+    (97, 0.25, 16, 0.5, "householder", 3),      # ragged: n not a multiple of any tile
+    (300, 0.5, 32, 0.35, "householder", 4),
+    (511, 0.0, 64, 0.6, "householder", 5),      # all 1x1 (Givens only)
+    (640, 100.0, 64, 0.3, "householder", 6),    # all 2x2 (Householder only)
+    (700, 0.25, 128, 0.35, "identity", 7),
+    (1000, 0.25, 256, 0.35, "householder", 8),  # several 256-row windows, ragged tails
+    (1200, 0.5, 200, 0.5, "none", 9),           # Q = NULL, w not a power of two
+    (64, 0.25, 4, 0.5, "householder", 10),      # smallest window
+    (130, 0.25, 5, 0.5, "householder", 11),     # odd window
+])
+def test_random_parity(n, p2, w, psel, q, seed):
+    p = make_problem(n, p2=p2, q=q, psel=psel, w=w, seed=seed)
+    S0, Q0, ref, got, Sg, Qg = run_both(p)
+    assert_parity(S0, Q0, ref, got, Sg, Qg, "n=%d w=%d" % (n, w))
+    check_reordering(S0, Q0, p.select, Sg, Qg, got["select"], got["m"], got["bmap"])
+
+
+def test_config1_parity():
+    """BASELINE config 1 (n = 4096, w = 128, random orthogonal Q), full oracle run."""
+    p = make_config(1, seed=1, device="cuda")
+    p.S = p.S.cpu(); p.Q = p.Q.cpu()
+    S0, Q0, ref, got, Sg, Qg = run_both(p)
+    assert_parity(S0, Q0, ref, got, Sg, Qg, "config1")
+    check_reordering(S0, Q0, p.select, Sg, Qg, got["select"], got["m"], got["bmap"])
+
+
+def test_block_diagonal_exact():
+    """Zero coupling: every transform is a signed (block) permutation, so the GPU result is
+    exact -- |entries| equal to the oracle's bitwise."""
+    p = make_problem(300, p2=0.25, q="householder", psel=0.4, w=32, seed=12)
+    S = p.S_np().copy(order="F")
+    bm = bmap_from_S(S)
+    mask = np.zeros_like(S, bool)
+    for r, sz in blocks_of(bm):
+        mask[r:r + sz, r:r + sz] = True
+    S[~mask] = 0.0
+    p.S = torch.from_numpy(np.ascontiguousarray(S.T))
+    S0, Q0, ref, got, Sg, Qg = run_both(p)
+    assert np.array_equal(np.abs(Sg), np.abs(ref["S"]))
+    assert np.array_equal(np.abs(Qg), np.abs(ref["Q"]))
+    np.testing.assert_array_equal(got["bmap"], ref["bmap"])
+
+
+def test_trivial_selections_bitwise_noop():
+    p = make_problem(500, q="householder", sel="all", w=64, seed=13)
+    for sel in (p.select, np.zeros_like(p.select)):
+        S = p.S.cuda(); Q = p.Q.cuda()
+        got = sn.reorder(S, Q, sel, window=64)
+        assert got["rc"] == 0 and got["stats"]["windows"] == 0
+        assert torch.equal(S.cpu(), p.S) and torch.equal(Q.cpu(), p.Q)
+
+
+def test_idempotent_second_call():
+    p = make_problem(800, q="householder", psel=0.35, w=128, seed=14)
+    S = p.S.cuda(); Q = p.Q.cuda()
+    r1 = sn.reorder(S, Q, p.select, window=128)
+    S1, Q1 = S.clone(), Q.clone()
+    r2 = sn.reorder(S, Q, r1["select"], window=128)
+    assert r2["rc"] == 0 and r2["stats"]["windows"] == 0
+    assert torch.equal(S, S1) and torch.equal(Q, Q1)
+
+
+def test_host_pointer_path_matches_device_path():
+    p = make_problem(777, q="householder", psel=0.35, w=128, seed=15)
+    Sd, Qd = p.S.cuda(), p.Q.cuda()
+    rd = sn.reorder(Sd, Qd, p.select, window=128)
+    Sh, Qh = p.S.clone(), p.Q.clone()
+    rh = sn.reorder(Sh, Qh, p.select, window=128)
+    assert rd["rc"] == rh["rc"] == 0
+    assert torch.equal(Sd.cpu(), Sh) and torch.equal(Qd.cpu(), Qh)
+    assert rh["stats"]["ms_h2d"] > 0
+
+
+def test_plain_abi_signature():
+    """sn_reorder_schur(n, S, ldS, Q, ldQ, select, &m) with raw device pointers."""
+    p = make_problem(256, q="householder", psel=0.5, w=64, seed=16)
+    S, Q = p.S.cuda(), p.Q.cuda()
+    sel = p.select.astype(np.int32).copy()
+    rc, m = sn.sn_reorder_schur(256, S.data_ptr(), 256, Q.data_ptr(), 256, sel)
+    torch.cuda.synchronize()
+    assert rc == 0 and m == int(p.select.sum())
+    check_reordering(p.S_np(), p.Q_np(), p.select, S.cpu().numpy().T, Q.cpu().numpy().T, sel, m,
+                     bmap_from_S(S.cpu().numpy().T))
+
+
+def test_edge_sizes():
+    for n in (1, 2, 3):
+        p = make_problem(n, p2=0.5, q="householder", psel=0.5, w=4, seed=17 + n)
+        S0, Q0, ref, got, Sg, Qg = run_both(p)
+        assert_parity(S0, Q0, ref, got, Sg, Qg, "n=%d" % n)
+
+
+def test_not_quasi_triangular_rejected():
+    p = make_problem(50, q="identity", psel=0.5, w=8, seed=20)
+    S = p.S.clone()
+    S[3, 10] = 1.0            # S[10, 3] != 0: below the subdiagonal
+    r = sn.reorder(S.cuda(), p.Q.cuda(), p.select, window=8, validate_lower=1)
+    assert r["rc"] == -2
+    S = p.S.clone()
+    S[4, 5] = 1.0; S[5, 6] = 1.0   # consecutive nonzero subdiagonal entries
+    r = sn.reorder(S.cuda(), p.Q.cuda(), p.select, window=8)
+    assert r["rc"] == -2
+
+
+def test_forced_rejection_consistent_state():
+    p = make_problem(600, p2=0.25, q="householder", psel=0.4, w=64, seed=21)
+    S, Q = p.S.cuda(), p.Q.cuda()
+    sch_full = sn.reorder(p.S.cuda(), p.Q.cuda(), p.select, window=64)
+    t = sch_full["stats"]["windows"] // 2
+    r = sn.reorder(S, Q, p.select, window=64, force_reject_window=t, force_reject_swap=3)
+    assert r["rc"] == sn.SN_ERR_REJECTED
+    assert r["stats"]["rejected_window"] == t
+    Sg, Qg = S.cpu().numpy().T, Q.cpu().numpy().T
+    n = p.n
+    A = p.Q_np() @ p.S_np() @ p.Q_np().T
+    assert np.linalg.norm(A - Qg @ Sg @ Qg.T) / np.linalg.norm(A) <= 100 * n * EPS
+    assert np.linalg.norm(Qg.T @ Qg - np.eye(n)) <= 100 * n * EPS
+    np.testing.assert_array_equal(r["bmap"], bmap_from_S(Sg))
+    assert int(r["select"].sum()) == r["m"]
+    row, n1 = r["stats"]["rejected_row"], r["stats"]["rejected_n1"]
+    assert r["select"][row + n1] == 1 and r["select"][row] == 0
+
+
+def test_prefix_parity_config2():
+    """BASELINE config 2 (n = 16384, w = 256): the first windows of the schedule on GPU and
+    oracle (SURVEY c5 'prefix parity'), compared over all of S and Q."""
+    p = make_config(2, seed=1, device="cuda")
+    K = 6
+    S0 = np.asfortranarray(p.S.cpu().numpy().T)
+    Q0 = np.asfortranarray(p.Q.cpu().numpy().T)
+    S, Q = p.S.clone(), p.Q.clone()
+    got = sn.reorder(S, Q, p.select, window=p.w, max_windows=K)
+    ref = oracle.reorder(S0, Q0, p.select, w=p.w, mode=1, max_windows=K)
+    assert got["rc"] == 0 == ref["rc"]
+    assert got["stats"]["windows"] == ref["stats"]["windows"] == K
+    np.testing.assert_array_equal(got["bmap"], ref["bmap"])
+    nS = np.linalg.norm(S0)
+    dS = np.abs(S.cpu().numpy().T - ref["S"]).max()
+    dQ = np.abs(Q.cpu().numpy().T - ref["Q"]).max()
+    print("config2 prefix K=%d: max|dS|/||S||=%.3g max|dQ|=%.3g" % (K, dS / nS, dQ))
+    assert dS <= TOL * nS and dQ <= TOL * nS
