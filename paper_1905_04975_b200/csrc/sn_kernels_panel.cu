@@ -10,7 +10,7 @@
 // place after its last K chunk is consumed (no other CTA touches it).  All three kinds are
 // the same product  C[m][x] = sum_kk Z[kk][m] * B[kk][x]  with A = Z^T from the Z slot and B
 // the strip (x = column for left, row for right/Q).  Operands are staged through shared
-// memory with a 3-stage cp.async pipeline and multiplied with mma.sync.m16n8k8.f64 (DMMA),
+// memory with a 3-stage cp.async pipeline and multiplied with mma.sync.m16n8k4.f64 (DMMA),
 // the FP64 tensor-core path of sm_100 (tcgen05 has no f64 kind).  DESIGN.md §6.
 #include <cstdint>
 
@@ -24,12 +24,11 @@ constexpr int KC = 16;        // K chunk
 constexpr int LDA = KC + 4;   // As[m][kk], row stride == 4 mod 16 (conflict-free fragments)
 constexpr int NSTAGE = 3;
 
-__device__ __forceinline__ void mma_16x8x8(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
+__device__ __forceinline__ void mma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
   asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
       : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
-      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+      : "d"(a0), "d"(a1), "d"(b0));
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -144,32 +143,26 @@ __global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
     cp_commit();
     const double* As = smem + (kc % NSTAGE) * C::STAGE;
     const double* Bs = As + C::A_ELEMS;
+    // k4-outer order: between two dependent DMMAs on one accumulator the warp issues
+    // MI*NI-1 independent ones (the m16n8k8 form chains two 8x8x4 DMMAs back to back).
 #pragma unroll
-    for (int ks = 0; ks < KC; ks += 8) {
-      double af[C::MI][4], bf[C::NI][2];
+    for (int ks = 0; ks < KC; ks += 4) {
+      double a0[C::MI], a1[C::MI], bf[C::NI];
 #pragma unroll
       for (int i = 0; i < C::MI; ++i) {
         const double* ap = As + (wm0 + i * 16 + g) * LDA + ks + t;
-        af[i][0] = ap[0];
-        af[i][1] = ap[8 * LDA];
-        af[i][2] = ap[4];
-        af[i][3] = ap[8 * LDA + 4];
+        a0[i] = ap[0];
+        a1[i] = ap[8 * LDA];
       }
 #pragma unroll
       for (int j = 0; j < C::NI; ++j) {
         const int xx = wn0 + j * 8 + g;
-        if (C::LEFT) {
-          bf[j][0] = Bs[xx * C::LDB + ks + t];
-          bf[j][1] = Bs[xx * C::LDB + ks + t + 4];
-        } else {
-          bf[j][0] = Bs[(ks + t) * C::LDB + xx];
-          bf[j][1] = Bs[(ks + t + 4) * C::LDB + xx];
-        }
+        bf[j] = C::LEFT ? Bs[xx * C::LDB + ks + t] : Bs[(ks + t) * C::LDB + xx];
       }
 #pragma unroll
       for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-        for (int j = 0; j < C::NI; ++j) mma_16x8x8(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < C::NI; ++j) mma_16x8x4(acc[i][j], a0[i], a1[i], bf[j]);
     }
   }
   cp_wait<0>();

@@ -4,8 +4,8 @@
 //
 // One CTA per window of a DAG level.  The window (k <= 256 rows) is processed as a chain of
 // inner windows of <= 64 rows (the plan's inner schedule): each inner window
-// is staged in shared memory, its block swaps run warp-cooperatively (sn_swap.cuh) into an
-// inner accumulator Zin, and Zin is then applied with FP64 DMMA (mma.sync m16n8k8 f64) to
+// is staged in shared memory, its block swaps run as a wavefront of movers (all 8 warps,
+// sn_swap.cuh) into an inner accumulator Zin, and Zin is then applied with FP64 DMMA (mma.sync m16n8k8 f64) to
 // the rest of the outer window and to the outer accumulator Z -- the paper's accumulated
 // level-3 update, one level down.  The outer Z is left in a 256x256 slot for
 // the panel kernels.
@@ -21,6 +21,10 @@ constexpr int kThreads = 256;
 constexpr int LDD = 65;   // inner window (odd stride: conflict-free row walks)
 constexpr int LDZ = 68;   // inner accumulator (== 4 mod 16: conflict-free DMMA fragments)
 constexpr int LDT = 68;   // staging tile
+
+// block list of the window being processed (one CTA per window)
+__shared__ uint8_t g_bsz[256], g_bsel[256];
+__shared__ int16_t g_brow[257];
 
 __device__ __forceinline__ void mma_16x8x8(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
   asm volatile(
@@ -115,14 +119,181 @@ __device__ void inner_update(double* P, int64_t ld, int64_t r0, int64_t c0, int 
   }
 }
 
+// ---- wavefront of movers inside one inner window ---------------------------------------
+// Mover i (i-th selected block of [top, bottom), top to bottom) starts at block P_i, passes
+// the u_i unselected blocks above it and ends at block top+i.  It performs its s-th swap at
+// step 2i + s, so concurrent swaps are at least two blocks apart: their index sets are
+// disjoint and their orthogonal factors commute.  Per step:
+//   A  transforms of all active swaps, one thread per swap, warp w <-> swap type w
+//   B  left applications (rows right of each block) + new diagonal blocks, a warp per swap
+//   C  right applications (columns above each block, accumulator columns), a warp per swap
+// with a CTA barrier after each phase.  Warp 0 prepares the next step's lists during C.
+struct WaveShared {
+  int M, U, T;                        // movers, unselected blocks, steps
+  uint8_t msz[64], usz[64];           // sizes of movers / unselected blocks (top to bottom)
+  int16_t mpos[64], mu[64];           // initial block position, unselected blocks above
+  int16_t mrows[65], urows[65];       // row prefixes of movers / unselected blocks
+  int16_t lj[2][4][32];               // per step parity, type, slot: local row j
+  int8_t lflat[2][4][32];             // ... flat index (mover order among active swaps)
+  int8_t ftype[2][64], fslot[2][64], fmover[2][64];
+  int cnt[2][4], nflat[2];
+  int8_t frej[64];
+  int anyrej, done, laststep;
+  int rej_row, rej_n1, rej_n2;
+};
+
+__device__ void wave_prepare(WaveShared& W, int t, int lane) {
+  // warp 0 only: lists of the active swaps of step t, grouped by type and in mover order
+  const int buf = t & 1;
+  const int i = lane;
+  bool act = false;
+  int ty = 0, j = 0;
+  if (i < W.M) {
+    const int s = t - 2 * i;
+    if (s >= 0 && s < W.mu[i]) {
+      act = true;
+      const int q = W.mu[i] - 1 - s;           // unselected block being passed
+      ty = (W.usz[q] - 1) * 2 + (W.msz[i] - 1);
+      j = W.mrows[i] + W.urows[q];
+    }
+  }
+  const unsigned amask = __ballot_sync(0xffffffffu, act);
+  const unsigned lt = (1u << lane) - 1u;
+  const int flat = __popc(amask & lt);
+  for (int q = 0; q < 4; ++q) {
+    const unsigned tm = __ballot_sync(0xffffffffu, act && ty == q);
+    if (act && ty == q) {
+      const int slot = __popc(tm & lt);
+      W.lj[buf][q][slot] = (int16_t)j;
+      W.lflat[buf][q][slot] = (int8_t)flat;
+      W.ftype[buf][flat] = (int8_t)q;
+      W.fslot[buf][flat] = (int8_t)slot;
+      W.fmover[buf][flat] = (int8_t)i;
+    }
+    if (lane == 0) W.cnt[buf][q] = __popc(tm);
+  }
+  if (lane == 0) W.nflat[buf] = __popc(amask);
+}
+
+__device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Din, double* Zin,
+                                WaveShared& W, int tid, int warp, int lane, bool force_here, int force_swap,
+                                int done_before) {
+  __shared__ double rec[4][32][dev::kRec];
+  if (tid == 0) {
+    // movers / unselected lists of the inner window (block list in s_bsz/s_bsel)
+    int M = 0, U = 0, T = 0;
+    W.mrows[0] = 0; W.urows[0] = 0;
+    for (int b = top; b < bottom; ++b) {
+      if (g_bsel[b]) {
+        W.msz[M] = g_bsz[b];
+        W.mpos[M] = (int16_t)b;
+        W.mu[M] = (int16_t)(b - top - M);
+        W.mrows[M + 1] = (int16_t)(W.mrows[M] + g_bsz[b]);
+        T = max(T, 2 * M + (b - top - M));
+        ++M;
+      } else {
+        W.usz[U] = g_bsz[b];
+        W.urows[U + 1] = (int16_t)(W.urows[U] + g_bsz[b]);
+        ++U;
+      }
+    }
+    W.M = M; W.U = U; W.T = T;
+    W.anyrej = 0; W.laststep = -1;
+    W.done = done_before;
+  }
+  __syncthreads();
+  if (warp == 0) wave_prepare(W, 0, lane);
+  __syncthreads();
+  const int T = W.T;
+  int t = 0;
+  for (; t < T; ++t) {
+    const int buf = t & 1;
+    const int base = W.done;
+    // A: transforms, one thread per swap
+    if (warp < 4 && lane < W.cnt[buf][warp]) {
+      const int j = W.lj[buf][warp][lane];
+      const int flat = W.lflat[buf][warp][lane];
+      bool rj = force_here && (base + flat == force_swap);
+      if (!rj) rj = dev::swap_compute_t(warp, Din, LDD, j, rec[warp][lane]);
+      W.frej[flat] = rj ? 1 : 0;
+      if (rj) atomicOr(&W.anyrej, 1);
+    }
+    __syncthreads();
+    const int nf = W.nflat[buf];
+    // B: rows
+    for (int f = warp; f < nf; f += kThreads / 32) {
+      if (W.frej[f]) continue;
+      const int ty = W.ftype[buf][f], sl = W.fslot[buf][f];
+      dev::swap_apply_rows_t(ty, Din, LDD, kin, W.lj[buf][ty][sl], rec[ty][sl], lane);
+    }
+    __syncthreads();
+    // C: columns of the window and of the accumulator
+    for (int f = warp; f < nf; f += kThreads / 32) {
+      if (W.frej[f]) continue;
+      const int ty = W.ftype[buf][f], sl = W.fslot[buf][f];
+      const int j = W.lj[buf][ty][sl];
+      dev::swap_apply_cols_t(ty, Din, LDD, j, j, rec[ty][sl], lane);
+      dev::swap_apply_cols_t(ty, Zin, LDZ, kin, j, rec[ty][sl], lane);
+    }
+    const bool stop = W.anyrej != 0;
+    if (warp == 0 && !stop && t + 1 < T) wave_prepare(W, t + 1, lane);
+    __syncthreads();
+    if (tid == 0) {
+      int nrej = 0, first = -1;
+      for (int f = 0; f < nf; ++f)
+        if (W.frej[f]) { ++nrej; if (first < 0) first = f; }
+      W.done += nf - nrej;
+      if (first >= 0) {
+        const int ty = W.ftype[buf][first], sl = W.fslot[buf][first];
+        W.rej_row = i1 + W.lj[buf][ty][sl];   // window-local row
+        W.rej_n1 = (ty >> 1) + 1;
+        W.rej_n2 = (ty & 1) + 1;
+      }
+      W.laststep = t;
+    }
+    __syncthreads();
+    if (stop) break;
+  }
+  // new block arrangement of [top, bottom)
+  if (tid == 0) {
+    uint8_t nsz[64], nsel[64];
+    int8_t occ[64];
+    const int nb = bottom - top;
+    for (int b = 0; b < nb; ++b) occ[b] = 0;
+    const int tl = W.laststep;
+    for (int i = 0; i < W.M; ++i) {
+      int applied = W.mu[i];
+      if (W.anyrej) {
+        applied = min(max(tl + 1 - 2 * i, 0), (int)W.mu[i]);
+        // a rejected swap of this mover at the last step was not applied
+        const int s = tl - 2 * i;
+        if (s >= 0 && s < W.mu[i]) {
+          const int buf = tl & 1;
+          for (int f = 0; f < W.nflat[buf]; ++f)
+            if (W.fmover[buf][f] == i && W.frej[f]) { applied -= 1; break; }
+        }
+      }
+      const int pos = W.mpos[i] - top - applied;
+      nsz[pos] = W.msz[i]; nsel[pos] = 1; occ[pos] = 1;
+    }
+    int q = 0;
+    for (int b = 0; b < nb; ++b)
+      if (!occ[b]) { nsz[b] = W.usz[q++]; nsel[b] = 0; }
+    for (int b = 0; b < nb; ++b) { g_bsz[top + b] = nsz[b]; g_bsel[top + b] = nsel[b]; }
+    for (int b = top; b < bottom; ++b) g_brow[b + 1] = (int16_t)(g_brow[b] + g_bsz[b]);
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
   extern __shared__ __align__(16) double smem[];
   double* Din = smem;                       // kInner x LDD
   double* Zin = Din + kInner * LDD;         // kInner x LDZ
   double* Tb = Zin + kInner * LDZ;          // 64 x LDT
-  __shared__ uint8_t bsz[256], bsel[256];
-  __shared__ int16_t brow[257];
-  __shared__ int s_rej, s_done_swaps, s_rej_row, s_rej_n1, s_rej_n2;
+  __shared__ WaveShared W;
+  uint8_t* bsz = g_bsz;
+  uint8_t* bsel = g_bsel;
+  int16_t* brow = g_brow;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int widx = blockIdx.x;
@@ -147,11 +318,9 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
     const int r = idx & (kZld - 1), c = idx >> 8;
     Z[idx] = (r == c && r < k) ? 1.0 : 0.0;
   }
-  if (tid == 0) {
-    s_rej = 0; s_done_swaps = 0;
-  }
   __syncthreads();
   if (tid == 0) {
+    W.anyrej = 0;
     int r = 0;
     for (int b = 0; b < nb; ++b) { brow[b] = (int16_t)r; r += bsz[b]; }
     brow[nb] = (int16_t)r;
@@ -170,42 +339,9 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
       Zin[r + c * LDZ] = (r == c && r < kin) ? 1.0 : 0.0;
     }
     __syncthreads();
-    if (warp == 0) {
-      // movers of [top, bottom) in top-to-bottom order; mover im ends at block top+im
-      int im = 0;
-      bool rej = false;
-      for (int b = top; b < bottom && !rej; ++b) {
-        if (!bsel[b]) continue;
-        for (int p = b; p > top + im; --p) {
-          const int jl = brow[p - 1] - i1;
-          const int n1 = bsz[p - 1], n2 = bsz[p];
-          bool r = (wd.order == a.force_order && swaps_done == a.force_swap);
-          if (!r) r = dev::warp_swap(Din, LDD, kin, jl, n1, n2, Zin, LDZ, kin, lane);
-          if (r) {
-            if (lane == 0) {
-              s_rej = 1;
-              s_rej_row = (int)(j1 + i1 + jl);
-              s_rej_n1 = n1;
-              s_rej_n2 = n2;
-            }
-            rej = true;
-            break;
-          }
-          ++swaps_done;
-          if (lane == 0) {
-            const uint8_t ts = bsz[p - 1], tl = bsel[p - 1];
-            bsz[p - 1] = bsz[p]; bsel[p - 1] = bsel[p];
-            bsz[p] = ts; bsel[p] = tl;
-            brow[p] = (int16_t)(brow[p - 1] + bsz[p - 1]);
-          }
-          __syncwarp();
-        }
-        ++im;
-      }
-      if (lane == 0) s_done_swaps = swaps_done;
-    }
-    __syncthreads();
-    swaps_done = s_done_swaps;
+    wavefront_swaps(top, bottom, i1, kin, Din, Zin, W, tid, warp, lane, wd.order == a.force_order,
+                    a.force_swap, swaps_done);
+    swaps_done = W.done;
     // write the inner window back
     for (int idx = tid; idx < kInner * kInner; idx += kThreads) {
       const int r = idx & (kInner - 1), c = idx >> 6;
@@ -216,16 +352,16 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
     inner_update<true>(S, ld, j1 + i1, j1 + i2, k - i2, kin, Zin, Tb, tid);      // cols right
     inner_update<false>(Z, kZld, 0, i1, k, kin, Zin, Tb, tid);                   // Z columns
     __syncthreads();
-    if (s_rej) break;
+    if (W.anyrej) break;
   }
   if (tid == 0) {
-    if (s_rej) {
+    if (W.anyrej) {
       a.ctl->abort = 1;
       a.ctl->rej_window = sidx;
       a.ctl->rej_swaps_done = swaps_done;
-      a.ctl->rej_row = s_rej_row;
-      a.ctl->rej_n1 = s_rej_n1;
-      a.ctl->rej_n2 = s_rej_n2;
+      a.ctl->rej_row = (int)(j1 + W.rej_row);
+      a.ctl->rej_n1 = W.rej_n1;
+      a.ctl->rej_n2 = W.rej_n2;
       for (int b = 0; b < nb; ++b) { a.ctl->rej_sz[b] = bsz[b]; a.ctl->rej_sel[b] = bsel[b]; }
       a.status[sidx] = kWinPartial;
     } else {

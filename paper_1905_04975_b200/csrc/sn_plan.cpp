@@ -157,6 +157,9 @@ int build_plan(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w, i
 }
 
 int64_t window_swaps(const Plan& P, int64_t t, int64_t cap, int64_t* sj, int8_t* s1, int8_t* s2) {
+  // Execution order of the window kernel: inner windows in order; inside one, the wavefront
+  // steps in order and, within a step, the active movers top to bottom (mover i makes its
+  // s-th swap at step 2i + s).
   if (t < 0 || t >= (int64_t)P.wins.size()) return -1;
   const WindowPlan& wp = P.wins[t];
   const uint8_t* base = P.pool.data() + wp.pool;
@@ -169,20 +172,35 @@ int64_t window_swaps(const Plan& P, int64_t t, int64_t cap, int64_t* sj, int8_t*
     const int top = inner[2 * q], bottom = inner[2 * q + 1];
     int64_t rtop = wp.j1;
     for (int b = 0; b < top; ++b) rtop += sz[b];
-    int im = 0;
+    std::vector<int> msz, usz, mu, mrows{0}, urows{0};
+    int T = 0;
     for (int b = top; b < bottom; ++b) {
-      if (!sel[b]) continue;
-      const int tgt = top + im;
-      for (int p = b; p > tgt; --p) {
-        int64_t r = rtop;
-        for (int x = top; x < p - 1; ++x) r += sz[x];
-        if (cnt < cap) { sj[cnt] = r; s1[cnt] = (int8_t)sz[p - 1]; s2[cnt] = (int8_t)sz[p]; }
-        ++cnt;
-        std::swap(sz[p - 1], sz[p]);
-        std::swap(sel[p - 1], sel[p]);
+      if (sel[b]) {
+        const int i = (int)msz.size();
+        msz.push_back(sz[b]);
+        mu.push_back(b - top - i);
+        mrows.push_back(mrows.back() + sz[b]);
+        T = std::max(T, 2 * i + mu.back());
+      } else {
+        usz.push_back(sz[b]);
+        urows.push_back(urows.back() + sz[b]);
       }
-      ++im;
     }
+    for (int step = 0; step < T; ++step)
+      for (int i = 0; i < (int)msz.size(); ++i) {
+        const int s = step - 2 * i;
+        if (s < 0 || s >= mu[i]) continue;
+        const int uq = mu[i] - 1 - s;
+        if (cnt < cap) {
+          sj[cnt] = rtop + mrows[i] + urows[uq];
+          s1[cnt] = (int8_t)usz[uq];
+          s2[cnt] = (int8_t)msz[i];
+        }
+        ++cnt;
+      }
+    int o = top;
+    for (int x : msz) { sz[o] = (uint8_t)x; sel[o] = 1; ++o; }
+    for (int x : usz) { sz[o] = (uint8_t)x; sel[o] = 0; ++o; }
   }
   return cnt;
 }
