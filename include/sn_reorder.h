@@ -59,6 +59,9 @@ typedef struct sn_opts {
                                 next level's window tasks */
   int32_t profile;           /* 1: bracket every kernel launch with CUDA events on its own
                                 stream and report per-kernel-kind times in sn_stats */
+  int32_t lookahead;         /* 1 (default): the next level's window kernel waits only for the
+                                update strips it reads; the rest overlaps it on a third stream */
+  int32_t reserved;
 } sn_opts;
 
 /* Statistics of one call. */
@@ -109,6 +112,13 @@ int sn_reorder_schur_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS, 
 int sn_schedule_build(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w,
                       int64_t* nwin, int64_t* nswap, int64_t* nlevels,
                       int64_t* win_j1, int64_t* win_k, int64_t* win_level, int64_t* win_nswap);
+
+/* Lookahead split of window t's update strips (width `strip` = 64 in the executor): the
+ * first crit_l[t] left-update strips and the last crit_r[t] right-update strips are applied
+ * before the next dependency level's window kernel; the others overlap it.
+ * Arrays of *nwin entries (schedule order).  Returns 0 or -i. */
+int sn_schedule_lookahead(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w, int64_t strip,
+                          int32_t* crit_l, int32_t* crit_r);
 
 /* The swaps of window t of the schedule above, in the library's execution order inside
  * the window (inner windows of `inner_window` rows): global row j, sizes n1 (block at j),

@@ -50,7 +50,7 @@ class Opts(C.Structure):
     _fields_ = [("window", C.c_int64), ("inner_window", C.c_int64), ("max_windows", C.c_int64),
                 ("force_reject_window", C.c_int64), ("force_reject_swap", C.c_int64),
                 ("validate_lower", C.c_int32), ("serialize", C.c_int32), ("q_stream_overlap", C.c_int32),
-                ("profile", C.c_int32)]
+                ("profile", C.c_int32), ("lookahead", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -73,7 +73,7 @@ class Stats(C.Structure):
 SN_OK, SN_ERR_REJECTED, SN_ERR_CUDA, SN_ERR_UNSUPPORTED = 0, 1, 2, 4
 
 EXPORTS = ["sn_default_opts", "sn_strerror", "sn_reorder_schur", "sn_reorder_schur_ex",
-           "sn_schedule_build", "sn_schedule_window_swaps", "sn_version"]
+           "sn_schedule_build", "sn_schedule_lookahead", "sn_schedule_window_swaps", "sn_version"]
 
 _lib = None
 
@@ -99,6 +99,8 @@ def lib():
         L.sn_schedule_build.argtypes = [i64, p, p, i64, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64),
                                         p, p, p, p]
         L.sn_schedule_build.restype = C.c_int
+        L.sn_schedule_lookahead.argtypes = [i64, p, p, i64, i64, p, p]
+        L.sn_schedule_lookahead.restype = C.c_int
         L.sn_schedule_window_swaps.argtypes = [i64, p, p, i64, i64, i64, i64, p, p, p]
         L.sn_schedule_window_swaps.restype = i64
         _lib = L
@@ -178,6 +180,19 @@ def schedule(bmap, selrow, w: int):
                         C.byref(nw), C.byref(ns), C.byref(nl), j1.ctypes.data_as(C.c_void_p),
                         k.ctypes.data_as(C.c_void_p), lev.ctypes.data_as(C.c_void_p), sw.ctypes.data_as(C.c_void_p))
     return {"j1": j1, "k": k, "level": lev, "nswap": sw, "nlevels": nl.value, "total_swaps": ns.value}
+
+
+def lookahead(bmap, selrow, w: int, strip: int = 64):
+    """Host-only: per window (schedule order) the critical left/right strip counts."""
+    bmap = np.ascontiguousarray(bmap, np.int8)
+    selrow = np.ascontiguousarray(selrow, np.int8)
+    nw = len(schedule(bmap, selrow, w)["j1"])
+    cl = np.zeros(nw, np.int32); cr = np.zeros(nw, np.int32)
+    rc = lib().sn_schedule_lookahead(len(bmap), bmap.ctypes.data_as(C.c_void_p), selrow.ctypes.data_as(C.c_void_p),
+                                     w, strip, cl.ctypes.data_as(C.c_void_p), cr.ctypes.data_as(C.c_void_p))
+    if rc:
+        raise ValueError("sn_schedule_lookahead rc=%d" % rc)
+    return cl, cr
 
 
 def window_swaps(bmap, selrow, w: int, t: int, inner_window: int = 64):

@@ -48,8 +48,9 @@ struct DevBuf {
 struct Workspace {
   DevBuf wins, pool, prefix, status, ctl, Z, sub, bad;
   std::vector<cudaEvent_t> prof;   // event pool for opts.profile
-  cudaStream_t sB = nullptr;
-  cudaEvent_t evW[kZgen] = {}, evQ[kZgen] = {}, ev0 = nullptr, ev1 = nullptr, evJoin = nullptr;
+  cudaStream_t sB = nullptr, sC = nullptr;
+  cudaEvent_t evW[kZgen] = {}, evQ[kZgen] = {}, evCrit[kZgen] = {}, evRest[kZgen] = {};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evJoin = nullptr, evJoinC = nullptr;
   int device = -1;
 };
 
@@ -77,17 +78,26 @@ int ensure_runtime(Workspace& ws) {
   if (ws.device != dev) {
     if (ws.sB) {
       cudaStreamDestroy(ws.sB);
-      for (int i = 0; i < kZgen; ++i) { cudaEventDestroy(ws.evW[i]); cudaEventDestroy(ws.evQ[i]); }
-      cudaEventDestroy(ws.ev0); cudaEventDestroy(ws.ev1); cudaEventDestroy(ws.evJoin);
+      cudaStreamDestroy(ws.sC);
+      for (int i = 0; i < kZgen; ++i) {
+        cudaEventDestroy(ws.evW[i]); cudaEventDestroy(ws.evQ[i]);
+        cudaEventDestroy(ws.evCrit[i]); cudaEventDestroy(ws.evRest[i]);
+      }
+      cudaEventDestroy(ws.ev0); cudaEventDestroy(ws.ev1);
+      cudaEventDestroy(ws.evJoin); cudaEventDestroy(ws.evJoinC);
     }
     CK(cudaStreamCreateWithFlags(&ws.sB, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ws.sC, cudaStreamNonBlocking));
     for (int i = 0; i < kZgen; ++i) {
       CK(cudaEventCreateWithFlags(&ws.evW[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&ws.evQ[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ws.evCrit[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ws.evRest[i], cudaEventDisableTiming));
     }
     CK(cudaEventCreate(&ws.ev0));
     CK(cudaEventCreate(&ws.ev1));
     CK(cudaEventCreateWithFlags(&ws.evJoin, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ws.evJoinC, cudaEventDisableTiming));
     ws.device = dev;
   }
   return 0;
@@ -188,27 +198,40 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   int64_t maxper = 0;
   for (int64_t l = 0; l < P.nlevels; ++l) maxper = std::max(maxper, lstart[l + 1] - lstart[l]);
   const int NT = 64;
+  constexpr int NK = 5;                // per level: 0 L-crit, 1 L-rest, 2 R-crit, 3 R-rest, 4 Q
   std::vector<WinDev> wd(nw);
-  std::vector<int32_t> pref;           // per level: 3 prefix arrays of (count+1)
-  std::vector<int64_t> pref_off(P.nlevels * 3);
-  std::vector<int32_t> nstrips(P.nlevels * 3);
+  std::vector<int32_t> pref;           // per level and kind: prefix over the level's windows
+  std::vector<int64_t> pref_off(P.nlevels * NK);
+  std::vector<int32_t> nstrips(P.nlevels * NK);
   double eq = 0.0;
+  const bool look = o.lookahead != 0;
+  std::vector<int32_t> critL(nw, 0), critR(nw, 0);
+  if (look) {
+    std::vector<int32_t> cl, cr;
+    lookahead_strips(P, NT, cl, cr);          // schedule order -> level-sorted order
+    for (int64_t i = 0; i < nw; ++i) { critL[i] = cl[sorted[i]]; critR[i] = cr[sorted[i]]; }
+  }
   for (int64_t l = 0; l < P.nlevels; ++l) {
     const int64_t a = lstart[l], b = lstart[l + 1];
-    for (int kind = 0; kind < 3; ++kind) {
-      pref_off[l * 3 + kind] = (int64_t)pref.size();
+    for (int kind = 0; kind < NK; ++kind) {
+      pref_off[l * NK + kind] = (int64_t)pref.size();
       int32_t acc = 0;
       pref.push_back(0);
       for (int64_t i = a; i < b; ++i) {
         const WindowPlan& w = P.wins[sorted[i]];
+        const int64_t nL = (n - (w.j1 + w.k) + NT - 1) / NT, nR = (w.j1 + NT - 1) / NT;
         int64_t cnt = 0;
-        if (kind == 0) cnt = (n - (w.j1 + w.k) + NT - 1) / NT;
-        else if (kind == 1) cnt = (w.j1 + NT - 1) / NT;
-        else cnt = Q ? (n + NT - 1) / NT : 0;
+        switch (kind) {
+          case 0: cnt = look ? critL[i] : nL; break;
+          case 1: cnt = look ? nL - critL[i] : 0; break;
+          case 2: cnt = look ? critR[i] : nR; break;
+          case 3: cnt = look ? nR - critR[i] : 0; break;
+          default: cnt = Q ? (n + NT - 1) / NT : 0; break;
+        }
         acc += (int32_t)cnt;
         pref.push_back(acc);
       }
-      nstrips[l * 3 + kind] = acc;
+      nstrips[l * NK + kind] = acc;
     }
     for (int64_t i = a; i < b; ++i) {
       const WindowPlan& w = P.wins[sorted[i]];
@@ -216,6 +239,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
       d.j1 = w.j1; d.k = w.k; d.nblk = w.nblk; d.ninner = w.ninner;
       d.slot = (int32_t)((l % kZgen) * maxper + (i - a));
       d.pool = w.pool; d.order = w.order;
+      d.crit_l = critL[i]; d.crit_r = critR[i];
     }
   }
   const double t_plan = now_ms();
@@ -260,6 +284,8 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   if (overlapQ) {
     CK(cudaStreamWaitEvent(ws.sB, ws.ev0, 0));
   }
+  cudaStream_t sC = look ? ws.sC : sA;
+  if (look) CK(cudaStreamWaitEvent(ws.sC, ws.ev0, 0));
   for (int64_t l = 0; l < P.nlevels; ++l) {
     const int64_t a = lstart[l], cnt = lstart[l + 1] - a;
     const int gen = (int)(l % kZgen);
@@ -279,21 +305,36 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     pa.wins = dw + a; pa.nwin = (int32_t)cnt; pa.base = (int32_t)a; pa.status = dstatus;
     pa.n = n; pa.Z = dZ;
     pa.M = S; pa.ld = ldS;
-    for (int kind = 0; kind < 2; ++kind) {
-      if (nstrips[l * 3 + kind] <= 0) continue;
-      pa.prefix = dpref + pref_off[l * 3 + kind];
-      pe = prof_begin(1 + kind, sA);
-      launch_panel(kind, mt, pa, nstrips[l * 3 + kind], sA);
-      prof_end(pe, sA);
+    // the strips of the previous level's rest may overlap this level's strips
+    if (look && l > 0) CK(cudaStreamWaitEvent(sA, ws.evRest[(l - 1) % kZgen], 0));
+    auto launch_part = [&](int kind, int part, int slot_kind, cudaStream_t s) -> int {
+      if (nstrips[l * NK + slot_kind] <= 0) return 0;
+      pa.prefix = dpref + pref_off[l * NK + slot_kind];
+      pa.part = look ? part : 0;
+      const int p2 = prof_begin(1 + kind, s);
+      launch_panel(kind, mt, pa, nstrips[l * NK + slot_kind], s);
+      prof_end(p2, s);
       launches[1 + kind]++;
-    }
+      return 0;
+    };
+    launch_part(0, 1, 0, sA);      // left, critical strips (all strips without lookahead)
+    launch_part(1, 1, 2, sA);      // right, critical strips
     CK(cudaGetLastError());
+    if (look) {
+      CK(cudaEventRecord(ws.evCrit[gen], sA));
+      CK(cudaStreamWaitEvent(sC, ws.evCrit[gen], 0));
+      launch_part(0, 2, 1, sC);    // left, remaining strips: overlap the next window kernel
+      launch_part(1, 2, 3, sC);
+      CK(cudaEventRecord(ws.evRest[gen], sC));
+      CK(cudaGetLastError());
+    }
     if (Q) {
       if (overlapQ) CK(cudaStreamWaitEvent(sQ, ws.evW[gen], 0));
       pa.M = Q; pa.ld = ldQ;
-      pa.prefix = dpref + pref_off[l * 3 + 2];
+      pa.prefix = dpref + pref_off[l * NK + 4];
+      pa.part = 0;
       pe = prof_begin(3, sQ);
-      launch_panel(2, mt, pa, nstrips[l * 3 + 2], sQ);
+      launch_panel(2, mt, pa, nstrips[l * NK + 4], sQ);
       prof_end(pe, sQ);
       launches[3]++;
       CK(cudaGetLastError());
@@ -302,11 +343,16 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     if (o.serialize) {
       CK(cudaStreamSynchronize(sA));
       if (overlapQ) CK(cudaStreamSynchronize(sQ));
+      if (look) CK(cudaStreamSynchronize(sC));
     }
   }
   if (overlapQ) {
     CK(cudaEventRecord(ws.evJoin, sQ));
     CK(cudaStreamWaitEvent(sA, ws.evJoin, 0));
+  }
+  if (look) {
+    CK(cudaEventRecord(ws.evJoinC, sC));
+    CK(cudaStreamWaitEvent(sA, ws.evJoinC, 0));
   }
   CK(cudaEventRecord(ws.ev1, sA));
   Control ctl;
@@ -427,6 +473,8 @@ void sn_default_opts(sn_opts* o) {
   o->validate_lower = 0;
   o->serialize = 0;
   o->q_stream_overlap = 1;
+  o->profile = 0;
+  o->lookahead = 1;
 }
 
 const char* sn_strerror(int code) {
@@ -527,6 +575,20 @@ int sn_schedule_build(int64_t n, const int8_t* bmap, const int8_t* selrow, int64
       if (win_nswap) win_nswap[t] = P.wins[t].nswap;
     }
   }
+  return 0;
+}
+
+int sn_schedule_lookahead(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w, int64_t strip,
+                          int32_t* crit_l, int32_t* crit_r) {
+  if (n < 0) return -1;
+  if (n > 0 && (!bmap || !selrow)) return -2;
+  if (strip < 1) return -5;
+  sn::Plan P;
+  int rc = sn::build_plan(n, bmap, selrow, w, 64, -1, &P);
+  if (rc) return rc;
+  std::vector<int32_t> cl, cr;
+  sn::lookahead_strips(P, strip, cl, cr);
+  for (size_t t = 0; t < cl.size(); ++t) { crit_l[t] = cl[t]; crit_r[t] = cr[t]; }
   return 0;
 }
 

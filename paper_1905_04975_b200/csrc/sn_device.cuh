@@ -18,6 +18,8 @@ struct WinDev {
   int32_t slot;      // Z slot
   int64_t pool;      // byte offset of sz[nblk], sel[nblk], (pad), inner[2*ninner] (uint16)
   int64_t order;     // schedule order
+  int32_t crit_l;    // left-update strips (a prefix) read by the next level's windows
+  int32_t crit_r;    // right-update strips (a suffix) read by the next level's windows
 };
 
 // Per-call device control block.
@@ -53,7 +55,8 @@ struct PanelArgs {
   const WinDev* wins;       // this level's windows
   int32_t nwin;
   int32_t base;
-  const int32_t* prefix;    // nwin+1 cumulative strip counts of this kind
+  const int32_t* prefix;    // nwin+1 cumulative strip counts of this kind and part
+  int32_t part;             // 0 all strips, 1 the critical strips, 2 the remaining strips
   const int32_t* status;
   double* M;                // S (left/right) or Q
   int64_t ld;

@@ -74,9 +74,13 @@ __global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
   const int w = lo;
   if (a.status[a.base + w] == kWinSkipped) return;
   const WinDev wd = a.wins[w];
-  const int strip = sid - a.prefix[w];
+  int strip = sid - a.prefix[w];
   const int k = wd.k;
   const int64_t j1 = wd.j1, ld = a.ld;
+  // critical strips (read by the next level's windows): a prefix of the left strips, a
+  // suffix of the right strips
+  if (KIND == 0 && a.part == 2) strip += wd.crit_l;
+  if (KIND == 1 && a.part == 1) strip += (int)((j1 + NT - 1) / NT) - wd.crit_r;
   double* M = a.M;
   const double* Z = a.Z + (int64_t)wd.slot * kZslot;
   int64_t x0;      // first column (left) or row (right/Q) of the strip

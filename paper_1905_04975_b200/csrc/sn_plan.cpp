@@ -3,7 +3,9 @@
 #include "sn_plan.h"
 
 #include <algorithm>
+#include <cstdint>
 #include <cstring>
+#include <utility>
 
 namespace sn {
 
@@ -154,6 +156,55 @@ int build_plan(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w, i
   }
   P.nlevels = maxlev + 1;
   return 0;
+}
+
+void lookahead_strips(const Plan& P, int64_t NT, std::vector<int32_t>& critL, std::vector<int32_t>& critR) {
+  const int64_t nw = (int64_t)P.wins.size(), n = P.n;
+  critL.assign(nw, 0);
+  critR.assign(nw, 0);
+  std::vector<std::vector<int64_t>> bylev(P.nlevels);
+  for (int64_t t = 0; t < nw; ++t) bylev[P.wins[t].level].push_back(t);
+  for (int64_t l = 0; l + 1 < P.nlevels; ++l) {
+    // the next level's windows are row-disjoint: find the one containing a given row
+    std::vector<std::pair<int64_t, int64_t>> nxt;   // (j1, j2), sorted
+    for (int64_t t : bylev[l + 1]) nxt.push_back({P.wins[t].j1, P.wins[t].j1 + P.wins[t].k});
+    std::sort(nxt.begin(), nxt.end());
+    auto containing = [&](int64_t r) -> int64_t {
+      auto it = std::upper_bound(nxt.begin(), nxt.end(), std::make_pair(r, INT64_MAX));
+      if (it == nxt.begin()) return -1;
+      --it;
+      return (r >= it->first && r < it->second) ? (int64_t)(it - nxt.begin()) : -1;
+    };
+    for (int64_t t : bylev[l]) {
+      const WindowPlan& x = P.wins[t];
+      const int64_t x1 = x.j1, x2 = x.j1 + x.k;
+      const int64_t nL = (n - x2 + NT - 1) / NT, nR = (x1 + NT - 1) / NT;
+      // left strips read by y: y contains row x2 and overlaps rows(x) -> columns [x2, y2)
+      int64_t q = x2 < n ? containing(x2) : -1;
+      if (q >= 0 && nxt[q].first < x2) critL[t] = (int32_t)std::min(nL, (nxt[q].second - x2 + NT - 1) / NT);
+      // right strips read by y: y contains row x1-1 and overlaps rows(x) -> rows [y1, x1)
+      q = x1 > 0 ? containing(x1 - 1) : -1;
+      if (q >= 0 && nxt[q].second > x1) critR[t] = (int32_t)(nR - nxt[q].first / NT);
+    }
+    // Closure.  Inside a level, the left update of a window a above a window b and the right
+    // update of b meet on rows(a) x cols(b); they commute only when each is applied whole
+    // there.  Critical right strips of b run before the remaining left strips, so if they
+    // touch rows(a), every left strip of a over cols(b) must be critical too (the critical
+    // left strips run first).
+    for (int64_t tb : bylev[l]) {
+      if (critR[tb] == 0) continue;
+      const WindowPlan& b = P.wins[tb];
+      const int64_t nRb = (b.j1 + NT - 1) / NT;
+      const int64_t cr0 = (nRb - critR[tb]) * NT;     // first row of b's critical right strips
+      for (int64_t ta : bylev[l]) {
+        const WindowPlan& a = P.wins[ta];
+        const int64_t a2 = a.j1 + a.k;
+        if (a2 > b.j1 || a2 <= cr0) continue;         // a not above b, or rows(a) untouched
+        const int64_t nLa = (n - a2 + NT - 1) / NT;
+        critL[ta] = (int32_t)std::max<int64_t>(critL[ta], std::min(nLa, (b.j1 + b.k - a2 + NT - 1) / NT));
+      }
+    }
+  }
 }
 
 int64_t window_swaps(const Plan& P, int64_t t, int64_t cap, int64_t* sj, int8_t* s1, int8_t* s2) {

@@ -45,6 +45,11 @@ struct Plan {
 int build_plan(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w, int64_t kin,
                int64_t max_windows, Plan* plan);
 
+// Lookahead split of the left/right update strips (strip width NT), per window in schedule
+// order: crit_l = leading left strips, crit_r = trailing right strips that must be applied
+// before the next level's window kernel.
+void lookahead_strips(const Plan& plan, int64_t NT, std::vector<int32_t>& crit_l, std::vector<int32_t>& crit_r);
+
 // Swap list of window t in kernel execution order (inner windows, movers top to bottom).
 int64_t window_swaps(const Plan& plan, int64_t t, int64_t cap, int64_t* sj, int8_t* s1, int8_t* s2);
 

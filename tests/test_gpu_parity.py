@@ -202,3 +202,13 @@ def test_prefix_parity_config2():
     dQ = np.abs(Q.cpu().numpy().T - ref["Q"]).max()
     print("config2 prefix K=%d: max|dS|/||S||=%.3g max|dQ|=%.3g" % (K, dS / nS, dQ))
     assert dS <= TOL * nS and dQ <= TOL * nS
+
+
+@pytest.mark.parametrize("opts", [dict(lookahead=0), dict(q_stream_overlap=0), dict(serialize=1),
+                                  dict(lookahead=0, q_stream_overlap=0, serialize=1), dict(inner_window=32),
+                                  dict(inner_window=16, lookahead=1)])
+def test_executor_variants_parity(opts):
+    """Every executor configuration (streams, lookahead, inner window size) meets the bar."""
+    p = make_problem(1500, p2=0.25, q="householder", psel=0.35, w=256, seed=30)
+    S0, Q0, ref, got, Sg, Qg = run_both(p, **opts)
+    assert_parity(S0, Q0, ref, got, Sg, Qg, str(opts))
