@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstdint>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -305,6 +306,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     pa.wins = dw + a; pa.nwin = (int32_t)cnt; pa.base = (int32_t)a; pa.status = dstatus;
     pa.n = n; pa.Z = dZ;
     pa.M = S; pa.ld = ldS;
+    pa.vec16 = (ldS % 2 == 0 && ((uintptr_t)S % 16) == 0) ? 1 : 0;
     // the strips of the previous level's rest may overlap this level's strips
     if (look && l > 0) CK(cudaStreamWaitEvent(sA, ws.evRest[(l - 1) % kZgen], 0));
     auto launch_part = [&](int kind, int part, int slot_kind, cudaStream_t s) -> int {
@@ -331,6 +333,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     if (Q) {
       if (overlapQ) CK(cudaStreamWaitEvent(sQ, ws.evW[gen], 0));
       pa.M = Q; pa.ld = ldQ;
+      pa.vec16 = (ldQ % 2 == 0 && ((uintptr_t)Q % 16) == 0) ? 1 : 0;
       pa.prefix = dpref + pref_off[l * NK + 4];
       pa.part = 0;
       pe = prof_begin(3, sQ);

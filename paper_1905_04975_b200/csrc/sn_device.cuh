@@ -57,6 +57,7 @@ struct PanelArgs {
   int32_t base;
   const int32_t* prefix;    // nwin+1 cumulative strip counts of this kind and part
   int32_t part;             // 0 all strips, 1 the critical strips, 2 the remaining strips
+  int32_t vec16;            // M is 16-byte aligned and ld is even: 16-byte row-strip copies
   const int32_t* status;
   double* M;                // S (left/right) or Q
   int64_t ld;

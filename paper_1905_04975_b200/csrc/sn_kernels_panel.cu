@@ -13,13 +13,13 @@
 // memory with a 3-stage cp.async pipeline and multiplied with mma.sync.m16n8k4.f64 (DMMA),
 // the FP64 tensor-core path of sm_100 (tcgen05 has no f64 kind).  DESIGN.md §6.
 #include <cstdint>
+#include <cstdlib>
 
 #include "sn_device.cuh"
 
 namespace sn {
 namespace {
 
-constexpr int kThreads = 256;
 constexpr int KC = 16;        // K chunk
 constexpr int LDA = KC + 4;   // As[m][kk], row stride == 4 mod 16 (conflict-free fragments)
 constexpr int NSTAGE = 3;
@@ -40,14 +40,18 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid
   const int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(sz));
 }
+__device__ __forceinline__ void cp_async16z(void* dst, const void* src, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
-template <int MT, int NT, int KIND>
+template <int MT, int NT, int KIND, int THREADS>
 struct Cfg {
   static constexpr bool LEFT = (KIND == 0);
-  static constexpr int WM = 4, WN = 2;
+  static constexpr int WN = 2, WM = THREADS / 32 / WN;
   static constexpr int MI = MT / (WM * 16);   // m16 tiles per warp
   static constexpr int NI = NT / (WN * 8);    // n8 tiles per warp
   static constexpr int LDB = LEFT ? (KC + 4) : (NT + 4);   // Bs[x][kk] (left) or Bs[kk][x]
@@ -57,9 +61,10 @@ struct Cfg {
   static constexpr size_t SMEM = sizeof(double) * (size_t)STAGE * NSTAGE;
 };
 
-template <int MT, int NT, int KIND>
-__global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
-  using C = Cfg<MT, NT, KIND>;
+template <int MT, int NT, int KIND, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) panel_kernel(PanelArgs a) {
+  using C = Cfg<MT, NT, KIND, THREADS>;
+  constexpr int kThreads = THREADS;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -111,6 +116,15 @@ __global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
         const bool v = (c < nx) && (kk0 + kk < k);
         const double* src = v ? M + (j1 + kk0 + kk) + (x0 + c) * ld : M;
         cp_async8(Bs + c * C::LDB + kk, src, v);
+      }
+    } else if (a.vec16) {
+      // Bs[kk][r..r+1] = M[(x0 + r) + (j1 + kk0 + kk)*ld], 16-byte copies (x0 is a multiple
+      // of NT, ld is even and M 16-byte aligned), zero-filled past the strip
+      for (int idx = tid; idx < NT * KC / 2; idx += kThreads) {
+        const int kk = idx / (NT / 2), r = 2 * (idx % (NT / 2));
+        const int nb = (kk0 + kk < k) ? 8 * max(0, min(2, nx - r)) : 0;
+        const double* src = nb ? M + (x0 + r) + (j1 + kk0 + kk) * ld : M;
+        cp_async16z(Bs + kk * C::LDB + r, src, nb);
       }
     } else {
       // Bs[kk][r] = M[(x0 + r) + (j1 + kk0 + kk)*ld]
@@ -190,22 +204,28 @@ __global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
       }
 }
 
-template <int MT, int NT, int KIND>
+template <int MT, int NT, int KIND, int THREADS>
 void launch_t(const PanelArgs& a, int32_t nstrips, cudaStream_t st) {
-  using C = Cfg<MT, NT, KIND>;
+  using C = Cfg<MT, NT, KIND, THREADS>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(panel_kernel<MT, NT, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaFuncSetAttribute(panel_kernel<MT, NT, KIND, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM);
     attr = true;
   }
-  panel_kernel<MT, NT, KIND><<<nstrips, kThreads, C::SMEM, st>>>(a);
+  panel_kernel<MT, NT, KIND, THREADS><<<nstrips, THREADS, C::SMEM, st>>>(a);
 }
 
 template <int KIND>
 void launch_kind(int mt, const PanelArgs& a, int32_t nstrips, cudaStream_t st) {
-  if (mt <= 64) launch_t<64, 64, KIND>(a, nstrips, st);
-  else if (mt <= 128) launch_t<128, 64, KIND>(a, nstrips, st);
-  else launch_t<256, 64, KIND>(a, nstrips, st);
+  static const int wide = [] {
+    const char* e = std::getenv("SN_PANEL_THREADS");
+    return e ? std::atoi(e) : 512;
+  }();
+  if (mt <= 64) launch_t<64, 64, KIND, 256>(a, nstrips, st);
+  else if (mt <= 128) launch_t<128, 64, KIND, 256>(a, nstrips, st);
+  else if (wide == 256) launch_t<256, 64, KIND, 256>(a, nstrips, st);
+  else launch_t<256, 64, KIND, 512>(a, nstrips, st);
 }
 
 }  // namespace

@@ -212,3 +212,25 @@ def test_executor_variants_parity(opts):
     p = make_problem(1500, p2=0.25, q="householder", psel=0.35, w=256, seed=30)
     S0, Q0, ref, got, Sg, Qg = run_both(p, **opts)
     assert_parity(S0, Q0, ref, got, Sg, Qg, str(opts))
+
+
+@pytest.mark.parametrize("pad", [1, 3])
+def test_padded_leading_dimension(pad):
+    """ldS = ldQ = n + pad (odd: the 8-byte copy paths; the buffers carry garbage padding)."""
+    p = make_problem(777, q="householder", psel=0.35, w=256, seed=31)
+    n, ld = p.n, p.n + pad
+    S0, Q0 = p.S_np().copy(order="F"), p.Q_np().copy(order="F")
+    ref = oracle.reorder(S0, Q0, p.select, w=256, mode=1)
+    Sb = torch.full((n, ld), float("nan"), dtype=torch.float64)
+    Qb = torch.full((n, ld), float("nan"), dtype=torch.float64)
+    Sb[:, :n] = p.S; Qb[:, :n] = p.Q
+    Sb, Qb = Sb.cuda(), Qb.cuda()
+    sel = p.select.astype(np.int32).copy()
+    rc, m = sn.sn_reorder_schur(n, Sb.data_ptr(), ld, Qb.data_ptr(), ld, sel)
+    torch.cuda.synchronize()
+    assert rc == 0 and m == ref["m"]
+    Sg, Qg = Sb[:, :n].cpu().numpy().T, Qb[:, :n].cpu().numpy().T
+    assert torch.isnan(Sb[:, n:]).all() and torch.isnan(Qb[:, n:]).all()
+    nS = np.linalg.norm(S0)
+    assert np.abs(Sg - ref["S"]).max() <= TOL * nS and np.abs(Qg - ref["Q"]).max() <= TOL * nS
+    np.testing.assert_array_equal(sel, ref["select"])
