@@ -209,14 +209,32 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
   for (; t < T; ++t) {
     const int buf = t & 1;
     const int base = W.done;
-    // A: transforms, one thread per swap
-    if (warp < 4 && lane < W.cnt[buf][warp]) {
+    // A: transforms, one thread per swap (a lane pair per 2x2|2x2 swap)
+    if (warp < 3 && lane < W.cnt[buf][warp]) {
       const int j = W.lj[buf][warp][lane];
       const int flat = W.lflat[buf][warp][lane];
       bool rj = force_here && (base + flat == force_swap);
       if (!rj) rj = dev::swap_compute_t(warp, Din, LDD, j, rec[warp][lane]);
       W.frej[flat] = rj ? 1 : 0;
       if (rj) atomicOr(&W.anyrej, 1);
+    } else if (warp == 3) {
+      const int c3 = W.cnt[buf][3];
+      for (int b0 = 0; b0 < c3; b0 += 16) {
+        const int slot = b0 + (lane >> 1), role = lane & 1;
+        const bool act = slot < c3;
+        const int sl = act ? slot : b0;
+        const int j = W.lj[buf][3][sl];
+        double tmp[dev::kRec];
+        bool rj = dev::swap_compute_22_paired(Din, LDD, j, tmp, role);
+        if (act && role == 0) {
+          const int flat = W.lflat[buf][3][slot];
+          rj = rj || (force_here && (base + flat == force_swap));
+#pragma unroll
+          for (int q = 0; q < dev::kRec; ++q) rec[3][slot][q] = tmp[q];
+          W.frej[flat] = rj ? 1 : 0;
+          if (rj) atomicOr(&W.anyrej, 1);
+        }
+      }
     }
     __syncthreads();
     const int nf = W.nflat[buf];

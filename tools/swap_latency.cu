@@ -22,6 +22,24 @@ __global__ void lat(const double* blk, long long* cyc, double* sink, int reps) {
   sink[0] = acc;
 }
 
+__global__ void lat22p(const double* blk, long long* cyc, double* sink, int reps) {
+  __shared__ double D[16];
+  if (threadIdx.x < 16) D[threadIdx.x] = blk[threadIdx.x];
+  __syncthreads();
+  double rec[32];
+  double acc = 0.0;
+  long long t0 = clock64();
+  for (int i = 0; i < reps; ++i) {
+    bool rj = sn::dev::swap_compute_22_paired(D, 4, 0, rec, threadIdx.x & 1);
+    acc += rec[0] + (rj ? 1.0 : 0.0);
+    __syncwarp();
+    if (threadIdx.x == 0) D[0] += acc * 1e-300;
+    __syncwarp();
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { cyc[0] = (t1 - t0) / reps; sink[0] = acc; }
+}
+
 int main() {
   // a 4x4 quasi-triangular block: [[a b . .],[c a . .],[0 0 e f],[0 0 g e]] etc.
   double h[16] = {2.0, -1.5, 0, 0,  1.2, 2.0, 0, 0,  0.3, -0.7, -3.0, 0.9,  0.4, 0.2, -1.1, -3.0};
@@ -43,5 +61,6 @@ int main() {
   run(h12, lat<1, 2>, "1x2");
   run(h21, lat<2, 1>, "2x1");
   run(h, lat<2, 2>, "2x2");
+  run(h, lat22p, "2x2_paired");
   return 0;
 }
