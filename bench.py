@@ -10,10 +10,13 @@ step starts from the same pristine input (restored by a device copy outside the 
 region).  Inputs (2 x 12.8 GB) exceed L2 (126 MB), so no extra flush is needed.
 
 metric: FP64 GFLOP/s of the equivalent update flops and wall seconds.
-Rank 0 prints one JSON line.  For N > 1 (torchrun), every rank runs an independent replica
-(the sharded multi-GPU layer is not built yet): scaling "weak", time = max
-over ranks.  --impl reference times the CPU oracle (oracle/, plain C, 1 core) on a bounded
-prefix of the same workload.
+Rank 0 prints one JSON line.  For N > 1 (torchrun, one process per GPU) the SAME problem is
+sharded over the ranks (sn_reorder_schur_dist: S column blocks of width
+--col-block, Q row blocks, each window's Z broadcast by NCCL): scaling "strong", time = max
+over ranks of the device time.  --emulate-ranks P runs the sharded program for P ranks on
+one GPU (sn_reorder_schur_dist_local; a measurement of the sharded path's overheads, not a
+multi-GPU number).  --impl reference times the CPU oracle (oracle/, plain C, 1 core) on a
+bounded prefix of the same workload.
 """
 from __future__ import annotations
 
@@ -173,6 +176,106 @@ def run_reference(args):
     return 0
 
 
+def run_sharded(args, ws, rank, local):
+    """N > 1: the sharded reordering of one problem over the ranks (strong scaling)."""
+    import paper_1905_04975_b200 as sn
+    from workloads import make_config
+    dev = torch.device("cuda", local)
+    prob = make_config(args.config, seed=args.seed, device=dev)
+    n, bc = prob.n, args.col_block
+    emu = ws == 1
+    P = args.emulate_ranks if emu else ws
+    ranks = list(range(P)) if emu else [rank]
+    shards = [sn.shard(prob.S, prob.Q, P, bc, r) for r in ranks]
+    S0 = [s for s, _ in shards]
+    Q0 = [q for _, q in shards]
+    del shards
+    prob.S = prob.Q = None
+    torch.cuda.empty_cache()
+    S = [x.clone() for x in S0]
+    Q = [x.clone() for x in Q0]
+    if not emu:
+        sn.dist_init(rank, ws, local)
+    stream = torch.cuda.current_stream(dev)
+
+    def call(Sl, Ql, **kw):
+        if emu:
+            return sn.reorder_dist_local(Sl, Ql, prob.select, n, bc, window=prob.w, stream=stream.cuda_stream, **kw)
+        return sn.reorder_dist(Sl[0], Ql[0], prob.select, n, bc, window=prob.w, stream=stream.cuda_stream, **kw)
+
+    def step():
+        for a, b in zip(S, S0):
+            a.copy_(b)
+        for a, b in zip(Q, Q0):
+            a.copy_(b)
+        torch.cuda.synchronize(dev)
+        barrier(ws)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = call(S, Q)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        assert r["rc"] == 0, r["rc"]
+        return e0.elapsed_time(e1), r
+
+    for _ in range(args.warmup):
+        step()
+    times, results = [], []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            ms, r = step()
+            times.append(ms)
+            results.append(r)
+    clocks = clk.summary()
+    tot_ms = allmax(ws, sum(times))
+    st = results[-1]["stats"]
+    eq = st["eq_flops"]
+    value = eq * args.steps / (tot_ms / 1000.0) / 1e9
+    gpu_launches = int(sum(sum(r["stats"]["launches"]) for r in results) / args.steps)
+    e2e = None
+    if args.e2e_steps > 0 and not emu:
+        Sh = torch.empty(S0[0].shape, dtype=torch.float64, pin_memory=True)
+        Qh = torch.empty(Q0[0].shape, dtype=torch.float64, pin_memory=True)
+        et = []
+        for _ in range(args.e2e_steps):
+            Sh.copy_(S0[0]); Qh.copy_(Q0[0])
+            torch.cuda.synchronize(dev)
+            barrier(ws)
+            t0 = time.perf_counter()
+            r = sn.reorder_dist(Sh, Qh, prob.select, n, bc, window=prob.w)
+            t1 = time.perf_counter()
+            assert r["rc"] == 0
+            et.append(t1 - t0)
+        e2e_s = allmax(ws, sum(et))
+        nb = 8 * (Sh.numel() + Qh.numel())
+        e2e = {"value": eq * args.e2e_steps / e2e_s / 1e9, "unit": "GFLOP/s", "wall_s": e2e_s / args.e2e_steps,
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "note": "per rank bytes (its shards)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "wall_s": tot_ms / args.steps / 1000.0,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": workload_desc(args.config, prob),
+                       "parallelism": ("emulated %d ranks on 1 GPU" % P) if emu else "sharded S col-blocks/Q row-blocks x%d" % ws,
+                       "col_block": bc,
+                       "l2": "inputs > 126 MB L2, no flush needed",
+                       "windows": st["windows"], "levels": st["levels"], "swaps": st["swaps"],
+                       "eq_tflop": eq / 1e12},
+            "roofline": None,
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    if not emu:
+        sn.dist_finalize()
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,6 +287,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--oracle-gflop", type=float, default=40.0, help="size of the oracle sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--col-block", type=int, default=512, help="column block width of the sharded S")
+    ap.add_argument("--emulate-ranks", type=int, default=0, help="sharded program for P ranks on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -193,6 +298,8 @@ def main():
     import paper_1905_04975_b200 as sn
     from workloads import make_config
     sn.lib()
+    if ws > 1 or args.emulate_ranks > 0:
+        return run_sharded(args, ws, rank, local)
     dev = torch.device("cuda", local)
     prob = make_config(args.config, seed=args.seed, device=dev)
     S0, Q0 = prob.S, prob.Q

@@ -27,6 +27,7 @@
  *     pointer, ld too small, -2 also when S is not upper quasi-triangular); SN_ERR_REJECTED
  *     (+1) a block swap failed the stability test: S and Q hold a valid, partially
  *     reordered Schur form and select/m describe it; SN_ERR_CUDA (+2) a CUDA error;
+ *     SN_ERR_NCCL (+3) an NCCL error or no communicator (sharded entry points);
  *     SN_ERR_UNSUPPORTED (+4) an option outside the supported range.
  *   - No CPU fallback: every arithmetic step runs in the library's CUDA kernels.  Without
  *     a usable CUDA device the compute entry points return SN_ERR_CUDA.
@@ -42,6 +43,7 @@ extern "C" {
 #define SN_OK 0
 #define SN_ERR_REJECTED 1
 #define SN_ERR_CUDA 2
+#define SN_ERR_NCCL 3
 #define SN_ERR_UNSUPPORTED 4
 
 /* Options (sn_default_opts fills the defaults). */
@@ -127,6 +129,52 @@ int sn_schedule_lookahead(int64_t n, const int8_t* bmap, const int8_t* selrow, i
 int64_t sn_schedule_window_swaps(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w,
                                  int64_t inner_window, int64_t t, int64_t cap,
                                  int64_t* swap_j, int8_t* swap_n1, int8_t* swap_n2);
+
+/* ---- sharded (multi-GPU) reordering; PAPER.md P:158 (concurrent windows),
+ * P:163-165 and P:189 (distributed blocks, implicit communication), P:249-258 ----
+ * One process per GPU.  S is distributed over column blocks of width col_block (bc >= w):
+ * global column j belongs to block b = j / bc on rank b % P and is stored, with all n rows,
+ * at local column (b / P) * bc + (j - b * bc) of S_loc (n x user_cols, ld ldS_loc >= n,
+ * user_cols from sn_dist_layout; columns past n in the last block are ignored).  Q is
+ * distributed over contiguous row blocks: rank r holds rows [q0, q1) of Q (sn_dist_layout)
+ * as Q_loc ((q1-q0) x n, ld ldQ_loc >= q1-q0), or Q_loc = NULL on every rank.  `select` is
+ * the full host int32[n] selection on every rank (in/out, identical on return); m, bmap_out
+ * and stats as for sn_reorder_schur_ex (stats count this rank's launches).  Per dependency
+ * level the window task runs on the owner of column j1, its Z is broadcast to all ranks
+ * (NCCL), every rank applies the left update to its own columns and the Q update to its own
+ * rows, the owner applies the right update; windows straddling a block boundary first pull
+ * the partner's columns [c, j2) (rows 0..j2) and push them back after the right update.
+ * Collective: every rank of the communicator must call it with the same n, col_block,
+ * options and selection.  Device or host shard pointers (host: staged inside the call). */
+
+/* NCCL unique id (128 bytes) for sn_dist_init; create on one rank, share by any means. */
+int sn_dist_unique_id(void* id_out);
+/* Create the library's NCCL communicator: rank of world, on CUDA device `device`. */
+int sn_dist_init(int rank, int world, const void* unique_id, int device);
+int sn_dist_finalize(void);
+/* Shard shapes of rank `rank`: S_loc columns, Q_loc rows [q0, q1).  Host only. */
+int sn_dist_layout(int64_t n, int64_t P, int64_t col_block, int64_t rank, int64_t* user_cols, int64_t* q0,
+                   int64_t* q1);
+int sn_reorder_schur_dist(const sn_opts* opts, int64_t n, int64_t col_block, double* S_loc, int64_t ldS_loc,
+                          double* Q_loc, int64_t ldQ_loc, int32_t* select, int64_t* m, int8_t* bmap_out,
+                          sn_stats* stats, void* stream);
+/* The same program for P ranks whose shards all live on the current device, executed in one
+ * process phase by phase (messages become device copies, the broadcast a shared buffer):
+ * the sharded data path on one GPU.  S_locs[r], Q_locs[r] (or Q_locs = NULL) as above. */
+int sn_reorder_schur_dist_local(const sn_opts* opts, int64_t P, int64_t n, int64_t col_block, double* const* S_locs,
+                                int64_t ldS_loc, double* const* Q_locs, int64_t ldQ_loc, int32_t* select,
+                                int64_t* m, int8_t* bmap_out, sn_stats* stats, void* stream);
+/* Host only: rank `rank`'s program as records of 8 int64 (returns the record count; pass
+ * rec = NULL to size).  The halo width is w.  Records:
+ *   (0, nlevels, nwin, ext_cols, q0, q1, hc, 0)                      header
+ *   (1, level, t, j1, k, owner, partner, coff)                       window (level-sorted)
+ *   (2, level, w0, w1, npull, nL, nR, nQ)                            level, then its
+ *   (3, w, src, dst, nrows, ncols, src_lcol, dst_lcol)  pulls, (4, wl, cnt, x0, 0..) L strips,
+ *   (5, ...) R strips, (7, ...) pushes, (6, ...) Q strips, in execution order.
+ * Local columns are in the extended layout: block lb at [lb*(bc+w), lb*(bc+w)+bc), its halo
+ * slot after it. */
+int64_t sn_dist_program(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w, int64_t col_block, int64_t P,
+                        int64_t rank, int64_t cap, int64_t* rec);
 
 /* Library version string. */
 const char* sn_version(void);

@@ -70,10 +70,12 @@ class Stats(C.Structure):
         return d
 
 
-SN_OK, SN_ERR_REJECTED, SN_ERR_CUDA, SN_ERR_UNSUPPORTED = 0, 1, 2, 4
+SN_OK, SN_ERR_REJECTED, SN_ERR_CUDA, SN_ERR_NCCL, SN_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 
 EXPORTS = ["sn_default_opts", "sn_strerror", "sn_reorder_schur", "sn_reorder_schur_ex",
-           "sn_schedule_build", "sn_schedule_lookahead", "sn_schedule_window_swaps", "sn_version"]
+           "sn_schedule_build", "sn_schedule_lookahead", "sn_schedule_window_swaps", "sn_version",
+           "sn_dist_unique_id", "sn_dist_init", "sn_dist_finalize", "sn_dist_layout", "sn_reorder_schur_dist",
+           "sn_reorder_schur_dist_local", "sn_dist_program"]
 
 _lib = None
 
@@ -103,6 +105,21 @@ def lib():
         L.sn_schedule_lookahead.restype = C.c_int
         L.sn_schedule_window_swaps.argtypes = [i64, p, p, i64, i64, i64, i64, p, p, p]
         L.sn_schedule_window_swaps.restype = i64
+        L.sn_dist_unique_id.argtypes = [p]
+        L.sn_dist_unique_id.restype = C.c_int
+        L.sn_dist_init.argtypes = [C.c_int, C.c_int, p, C.c_int]
+        L.sn_dist_init.restype = C.c_int
+        L.sn_dist_finalize.restype = C.c_int
+        L.sn_dist_layout.argtypes = [i64, i64, i64, i64, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
+        L.sn_dist_layout.restype = C.c_int
+        L.sn_reorder_schur_dist.argtypes = [C.POINTER(Opts), i64, i64, p, i64, p, i64, p, C.POINTER(i64), p,
+                                            C.POINTER(Stats), p]
+        L.sn_reorder_schur_dist.restype = C.c_int
+        L.sn_reorder_schur_dist_local.argtypes = [C.POINTER(Opts), i64, i64, i64, p, i64, p, i64, p, C.POINTER(i64),
+                                                  p, C.POINTER(Stats), p]
+        L.sn_reorder_schur_dist_local.restype = C.c_int
+        L.sn_dist_program.argtypes = [i64, p, p, i64, i64, i64, i64, i64, p]
+        L.sn_dist_program.restype = i64
         _lib = L
     return _lib
 
@@ -207,3 +224,140 @@ def window_swaps(bmap, selrow, w: int, t: int, inner_window: int = 64):
     if cnt < 0:
         raise ValueError("sn_schedule_window_swaps rc=%d" % cnt)
     return sj[:cnt], s1[:cnt], s2[:cnt]
+
+
+# ---- sharded (multi-GPU) reordering: include/sn_reorder.h "sharded" section ----------------
+
+def dist_layout(n: int, P: int, col_block: int, rank: int):
+    """(user_cols, q0, q1): this rank's S_loc columns and Q row range (host only)."""
+    uc, q0, q1 = C.c_int64(), C.c_int64(), C.c_int64()
+    rc = lib().sn_dist_layout(n, P, col_block, rank, C.byref(uc), C.byref(q0), C.byref(q1))
+    if rc:
+        raise ValueError("sn_dist_layout rc=%d" % rc)
+    return uc.value, q0.value, q1.value
+
+
+def owned_columns(n: int, P: int, col_block: int, rank: int) -> np.ndarray:
+    """Global columns of rank's blocks in local (compact layout) order."""
+    nb = (n + col_block - 1) // col_block
+    return np.concatenate([np.arange(b * col_block, min(n, (b + 1) * col_block)) for b in range(rank, nb, P)]
+                          or [np.zeros(0, np.int64)]).astype(np.int64)
+
+
+def shard(S, Q, P: int, col_block: int, rank: int):
+    """Rank's shards of full S, Q (torch tensors holding the column-major matrices, as in
+    reorder()): S_loc (user_cols, n) and Q_loc (n, ceil(n/P)) tensors whose memory is the
+    column-major n x user_cols block columns and (q1-q0) x n row block (ld ceil(n/P))."""
+    import torch
+    n = S.shape[0]
+    uc, q0, q1 = dist_layout(n, P, col_block, rank)
+    cols = owned_columns(n, P, col_block, rank)
+    Sl = torch.zeros((max(uc, 1), n), dtype=S.dtype, device=S.device)
+    if len(cols):
+        Sl[:len(cols)] = S[torch.as_tensor(cols, device=S.device)]
+    Ql = None
+    if Q is not None:
+        # every rank's Q_loc has ld = ceil(n/P) (the last row block may be shorter)
+        Ql = torch.zeros((n, max(1, -(-n // P))), dtype=Q.dtype, device=Q.device)
+        Ql[:, :q1 - q0] = Q[:, q0:q1]
+    return Sl, Ql
+
+
+def unshard(S_locs, Q_locs, n: int, P: int, col_block: int):
+    """Inverse of shard() over all ranks (numpy, column-major matrices as 2-D arrays)."""
+    S = np.zeros((n, n))
+    Q = None if Q_locs is None else np.zeros((n, n))
+    for r in range(P):
+        cols = owned_columns(n, P, col_block, r)
+        Sl = S_locs[r].cpu().numpy() if hasattr(S_locs[r], "cpu") else S_locs[r]
+        S[:, cols] = Sl[:len(cols)].T
+        if Q is not None:
+            _, q0, q1 = dist_layout(n, P, col_block, r)
+            Ql = Q_locs[r].cpu().numpy() if hasattr(Q_locs[r], "cpu") else Q_locs[r]
+            Q[q0:q1, :] = Ql.T[:q1 - q0]
+    return S, Q
+
+
+def reorder_dist_local(S_locs, Q_locs, select, n: int, col_block: int, window: int = 256, stream=None, **opts):
+    """The sharded program for len(S_locs) ranks whose shards all live on the current device
+    (sn_reorder_schur_dist_local).  Shards as produced by shard(); modified in place."""
+    import torch
+    P = len(S_locs)
+    sp = (C.c_void_p * P)(*[C.c_void_p(t.data_ptr()) for t in S_locs])
+    qp = None if Q_locs is None else (C.c_void_p * P)(*[C.c_void_p(t.data_ptr()) for t in Q_locs])
+    ldq = 1
+    if Q_locs is not None:
+        ldq = max(1, max(t.shape[1] for t in Q_locs))
+        for t in Q_locs:
+            assert t.shape[1] == ldq, "Q shards must share one leading dimension (see shard())"
+    o = default_opts(window=window, **opts)
+    sel = np.ascontiguousarray(select, np.int32).copy()
+    bmap = np.zeros(n, np.int8)
+    m = C.c_int64()
+    st = Stats()
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
+    rc = lib().sn_reorder_schur_dist_local(C.byref(o), P, n, col_block, sp, n, qp, ldq,
+                                           sel.ctypes.data_as(C.c_void_p), C.byref(m),
+                                           bmap.ctypes.data_as(C.c_void_p), C.byref(st), C.c_void_p(stream))
+    return {"rc": rc, "m": m.value, "select": sel, "bmap": bmap, "stats": st.to_dict()}
+
+
+def dist_init(rank: int, world: int, device: int, broadcast_id=None):
+    """Create the library's NCCL communicator.  broadcast_id(bytes) -> bytes shares rank 0's
+    unique id (default: torch.distributed.broadcast_object_list on the default group)."""
+    buf = (C.c_char * 128)()
+    if rank == 0:
+        rc = lib().sn_dist_unique_id(buf)
+        if rc:
+            raise RuntimeError("sn_dist_unique_id rc=%d (%s)" % (rc, strerror(rc)))
+    raw = bytes(buf)
+    if broadcast_id is None:
+        import torch.distributed as dist
+        obj = [raw]
+        dist.broadcast_object_list(obj, src=0)
+        raw = obj[0]
+    else:
+        raw = broadcast_id(raw)
+    buf = (C.c_char * 128).from_buffer_copy(raw)
+    rc = lib().sn_dist_init(rank, world, buf, device)
+    if rc:
+        raise RuntimeError("sn_dist_init rc=%d (%s)" % (rc, strerror(rc)))
+
+
+def dist_finalize():
+    lib().sn_dist_finalize()
+
+
+def reorder_dist(S_loc, Q_loc, select, n: int, col_block: int, window: int = 256, stream=None, **opts):
+    """This rank's part of the sharded reordering (sn_reorder_schur_dist; collective)."""
+    import torch
+    o = default_opts(window=window, **opts)
+    sel = np.ascontiguousarray(select, np.int32).copy()
+    bmap = np.zeros(n, np.int8)
+    m = C.c_int64()
+    st = Stats()
+    ldq = 1 if Q_loc is None else max(1, Q_loc.shape[1])
+    if stream is None and S_loc.is_cuda:
+        stream = torch.cuda.current_stream(S_loc.device).cuda_stream
+    rc = lib().sn_reorder_schur_dist(C.byref(o), n, col_block, C.c_void_p(S_loc.data_ptr()), n,
+                                     None if Q_loc is None else C.c_void_p(Q_loc.data_ptr()), ldq,
+                                     sel.ctypes.data_as(C.c_void_p), C.byref(m), bmap.ctypes.data_as(C.c_void_p),
+                                     C.byref(st), None if stream is None else C.c_void_p(stream))
+    return {"rc": rc, "m": m.value, "select": sel, "bmap": bmap, "stats": st.to_dict()}
+
+
+def dist_program(bmap, selrow, w: int, col_block: int, P: int, rank: int) -> np.ndarray:
+    """Host only: rank's sharded program as an (R, 8) int64 record array (sn_reorder.h)."""
+    bmap = np.ascontiguousarray(bmap, np.int8)
+    selrow = np.ascontiguousarray(selrow, np.int8)
+    n = len(bmap)
+    L = lib()
+    cnt = L.sn_dist_program(n, bmap.ctypes.data_as(C.c_void_p), selrow.ctypes.data_as(C.c_void_p), w, col_block,
+                            P, rank, 0, None)
+    if cnt < 0:
+        raise ValueError("sn_dist_program rc=%d" % cnt)
+    rec = np.zeros((cnt, 8), np.int64)
+    L.sn_dist_program(n, bmap.ctypes.data_as(C.c_void_p), selrow.ctypes.data_as(C.c_void_p), w, col_block, P, rank,
+                      cnt, rec.ctypes.data_as(C.c_void_p))
+    return rec

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "sn_device.cuh"
+#include "sn_exec.h"
 #include "sn_plan.h"
 #include "sn_reorder.h"
 
@@ -56,6 +57,9 @@ struct Workspace {
 };
 
 Workspace g_ws;
+
+}  // namespace
+
 std::mutex g_mu;
 
 double now_ms() {
@@ -73,7 +77,7 @@ double now_ms() {
     }                                                                  \
   } while (0)
 
-int ensure_runtime(Workspace& ws) {
+static int ensure_runtime(Workspace& ws) {
   int dev = 0;
   CK(cudaGetDevice(&dev));
   if (ws.device != dev) {
@@ -114,7 +118,7 @@ bool is_device_ptr(const void* p) {
 }
 
 // movers-first stable partition of a block range
-void partition(std::vector<uint8_t>& sz, std::vector<uint8_t>& sel, int64_t top, int64_t nb,
+static void partition(std::vector<uint8_t>& sz, std::vector<uint8_t>& sel, int64_t top, int64_t nb,
                const uint8_t* psz, const uint8_t* psel) {
   int64_t o = top;
   for (int64_t b = 0; b < nb; ++b)
@@ -122,6 +126,84 @@ void partition(std::vector<uint8_t>& sz, std::vector<uint8_t>& sel, int64_t top,
   for (int64_t b = 0; b < nb; ++b)
     if (!psel[b]) { sz[o] = psz[b]; sel[o] = 0; ++o; }
 }
+
+
+int structure_from_sub(int64_t n, const uint8_t* sub, const int32_t* select, int8_t* bmap, int8_t* selrow,
+                       int64_t* m) {
+  int64_t msel = 0;
+  for (int64_t i = 0; i < n;) {
+    if (sub[i]) {
+      if (i + 2 < n && sub[i + 1]) return -2;   // two consecutive nonzero subdiagonal entries
+      bmap[i] = 1; bmap[i + 1] = 2;
+      const int8_t s = (select[i] != 0 || select[i + 1] != 0) ? 1 : 0;
+      selrow[i] = selrow[i + 1] = s;
+      msel += 2 * s;
+      i += 2;
+    } else {
+      bmap[i] = 0;
+      selrow[i] = select[i] != 0 ? 1 : 0;
+      msel += selrow[i];
+      i += 1;
+    }
+  }
+  *m = msel;
+  return 0;
+}
+
+void final_blocks(const Plan& P, const std::vector<int64_t>& sorted, const Control& ctl, const int32_t* status,
+                  int64_t n, const int8_t* bmap, const int8_t* selrow, std::vector<uint8_t>& fsz,
+                  std::vector<uint8_t>& fsel, int64_t* executed_out, int64_t* swaps_out, int64_t sbt[4]) {
+  const int64_t nw = (int64_t)P.wins.size();
+  int64_t executed = nw, swaps = 0;
+  if (!ctl.abort) {
+    fsz = P.final_sz; fsel = P.final_sel;
+    for (const auto& w : P.wins) {
+      swaps += w.nswap;
+      for (int q = 0; q < 4; ++q) sbt[q] += w.swaps_by_type[q];
+    }
+  } else {
+    fsz.clear(); fsel.clear();
+    for (int64_t i = 0; i < n;) {
+      const int s = bmap[i] == 1 ? 2 : 1;
+      fsz.push_back((uint8_t)s); fsel.push_back((uint8_t)selrow[i]);
+      i += s;
+    }
+    std::vector<int64_t> pos_of(nw);
+    for (int64_t i = 0; i < nw; ++i) pos_of[sorted[i]] = i;
+    executed = 0;
+    for (int64_t t = 0; t < nw; ++t) {
+      const WindowPlan& w = P.wins[t];
+      const int32_t stt = status[pos_of[t]];
+      if (stt == kWinDone) {
+        partition(fsz, fsel, w.top, w.nblk, P.pool.data() + w.pool, P.pool.data() + w.pool + w.nblk);
+        swaps += w.nswap;
+        for (int q = 0; q < 4; ++q) sbt[q] += w.swaps_by_type[q];
+        ++executed;
+      } else if (stt == kWinPartial) {
+        std::memcpy(fsz.data() + w.top, ctl.rej_sz, (size_t)w.nblk);
+        std::memcpy(fsel.data() + w.top, ctl.rej_sel, (size_t)w.nblk);
+        swaps += ctl.rej_swaps_done;
+        ++executed;
+      }
+    }
+  }
+  *executed_out = executed;
+  *swaps_out = swaps;
+}
+
+void write_blocks(const std::vector<uint8_t>& fsz, const std::vector<uint8_t>& fsel, int32_t* select,
+                  int8_t* bmap_out) {
+  int64_t r = 0;
+  for (size_t b = 0; b < fsz.size(); ++b) {
+    for (int q = 0; q < fsz[b]; ++q) {
+      select[r + q] = fsel[b];
+      if (bmap_out) bmap_out[r + q] = (int8_t)(fsz[b] == 1 ? 0 : 1 + q);
+    }
+    r += fsz[b];
+  }
+}
+
+namespace {
 
 int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ, int32_t* select,
         int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA) {
@@ -166,23 +248,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   CK(cudaStreamSynchronize(sA));
   if (bad) return -2;
   std::vector<int8_t> bmap((size_t)n), selrow((size_t)n);
-  int64_t msel = 0;
-  for (int64_t i = 0; i < n;) {
-    if (sub[i]) {
-      if (i + 2 < n && sub[i + 1]) return -2;   // two consecutive nonzero subdiagonal entries
-      bmap[i] = 1; bmap[i + 1] = 2;
-      const int8_t s = (select[i] != 0 || select[i + 1] != 0) ? 1 : 0;
-      selrow[i] = selrow[i + 1] = s;
-      msel += 2 * s;
-      i += 2;
-    } else {
-      bmap[i] = 0;
-      selrow[i] = select[i] != 0 ? 1 : 0;
-      msel += selrow[i];
-      i += 1;
-    }
-  }
-  *m = msel;
+  if (int rc = structure_from_sub(n, sub.data(), select, bmap.data(), selrow.data(), m)) return rc;
 
   // ---- a2: plan (window schedule, inner schedules, DAG levels)
   Plan P;
@@ -204,7 +270,6 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   std::vector<int32_t> pref;           // per level and kind: prefix over the level's windows
   std::vector<int64_t> pref_off(P.nlevels * NK);
   std::vector<int32_t> nstrips(P.nlevels * NK);
-  double eq = 0.0;
   const bool look = o.lookahead != 0;
   std::vector<int32_t> critL(nw, 0), critR(nw, 0);
   if (look) {
@@ -241,6 +306,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
       d.slot = (int32_t)((l % kZgen) * maxper + (i - a));
       d.pool = w.pool; d.order = w.order;
       d.crit_l = critL[i]; d.crit_r = critR[i];
+      d.coff = 0; d.sidx = (int32_t)i; d.pad = 0;
     }
   }
   const double t_plan = now_ms();
@@ -291,7 +357,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     const int64_t a = lstart[l], cnt = lstart[l + 1] - a;
     const int gen = (int)(l % kZgen);
     if (overlapQ && l >= kZgen) CK(cudaStreamWaitEvent(sA, ws.evQ[gen], 0));
-    WindowArgs wa;
+    WindowArgs wa{};
     wa.wins = dw + a; wa.nwin = (int32_t)cnt; wa.base = (int32_t)a;
     wa.pool = (const uint8_t*)ws.pool.p; wa.S = S; wa.ldS = ldS; wa.Z = dZ;
     wa.status = dstatus; wa.ctl = dctl;
@@ -302,7 +368,8 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     launches[0]++;
     CK(cudaGetLastError());
     if (overlapQ) CK(cudaEventRecord(ws.evW[gen], sA));
-    PanelArgs pa;
+    PanelArgs pa{};
+    pa.strips = nullptr;
     pa.wins = dw + a; pa.nwin = (int32_t)cnt; pa.base = (int32_t)a; pa.status = dstatus;
     pa.n = n; pa.Z = dZ;
     pa.M = S; pa.ld = ldS;
@@ -370,39 +437,12 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   int64_t executed = nw, swaps = 0;
   double eqf = 0.0;
   int64_t sbt[4] = {0, 0, 0, 0};
-  if (!ctl.abort) {
-    fsz = P.final_sz; fsel = P.final_sel;
-    for (const auto& w : P.wins) {
-      swaps += w.nswap;
-      for (int q = 0; q < 4; ++q) sbt[q] += w.swaps_by_type[q];
-    }
-  } else {
+  if (ctl.abort) {
     status.resize(nw);
     CK(cudaMemcpy(status.data(), dstatus, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < n;) {
-      const int s = bmap[i] == 1 ? 2 : 1;
-      fsz.push_back((uint8_t)s); fsel.push_back((uint8_t)selrow[i]);
-      i += s;
-    }
-    std::vector<int64_t> pos_of(nw);
-    for (int64_t i = 0; i < nw; ++i) pos_of[sorted[i]] = i;
-    executed = 0;
-    for (int64_t t = 0; t < nw; ++t) {
-      const WindowPlan& w = P.wins[t];
-      const int32_t stt = status[pos_of[t]];
-      if (stt == kWinDone) {
-        partition(fsz, fsel, w.top, w.nblk, P.pool.data() + w.pool, P.pool.data() + w.pool + w.nblk);
-        swaps += w.nswap;
-        for (int q = 0; q < 4; ++q) sbt[q] += w.swaps_by_type[q];
-        ++executed;
-      } else if (stt == kWinPartial) {
-        std::memcpy(fsz.data() + w.top, ctl.rej_sz, (size_t)w.nblk);
-        std::memcpy(fsel.data() + w.top, ctl.rej_sel, (size_t)w.nblk);
-        swaps += ctl.rej_swaps_done;
-        ++executed;
-      }
-    }
   }
+  final_blocks(P, sorted, ctl, ctl.abort ? status.data() : nullptr, n, bmap.data(), selrow.data(), fsz, fsel,
+               &executed, &swaps, sbt);
   double fk[5] = {0, 0, 0, 0, 0}, bk[5] = {0, 0, 0, 0, 0};
   for (int64_t i = 0; i < nw; ++i) {
     const WindowPlan& w = P.wins[sorted[i]];
@@ -420,17 +460,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ws.prof[pm.second], ws.prof[pm.second + 1]) == cudaSuccess) mk[pm.first] += ms;
   }
-  (void)eq;
-  {
-    int64_t r = 0;
-    for (size_t b = 0; b < fsz.size(); ++b) {
-      for (int q = 0; q < fsz[b]; ++q) {
-        select[r + q] = fsel[b];
-        if (bmap_out) bmap_out[r + q] = (int8_t)(fsz[b] == 1 ? 0 : 1 + q);
-      }
-      r += fsz[b];
-    }
-  }
+  write_blocks(fsz, fsel, select, bmap_out);
   if (st) {
     std::memset(st, 0, sizeof(*st));
     st->windows = executed;

@@ -20,6 +20,18 @@ struct WinDev {
   int64_t order;     // schedule order
   int32_t crit_l;    // left-update strips (a prefix) read by the next level's windows
   int32_t crit_r;    // right-update strips (a suffix) read by the next level's windows
+  int64_t coff;      // column offset: column j of S is stored at column j + coff of the
+                     // array passed (0 on one GPU; the extended local layout when sharded)
+  int32_t sidx;      // index of this window in the status array (level-sorted order)
+  int32_t pad;
+};
+
+// One panel strip given explicitly (the sharded executor, sn_dist.h): window index within
+// the level, columns (left) or rows (right, Q), and the first column / row.
+struct StripDev {
+  int32_t w;
+  int32_t cnt;
+  int64_t x0;
 };
 
 // Per-call device control block.
@@ -56,6 +68,7 @@ struct PanelArgs {
   int32_t nwin;
   int32_t base;
   const int32_t* prefix;    // nwin+1 cumulative strip counts of this kind and part
+  const StripDev* strips;   // explicit strips (sharded executor); prefix unused if set
   int32_t part;             // 0 all strips, 1 the critical strips, 2 the remaining strips
   int32_t vec16;            // M is 16-byte aligned and ld is even: 16-byte row-strip copies
   const int32_t* status;
@@ -68,6 +81,9 @@ struct PanelArgs {
 // kernel launchers (sn_kernels_*.cu)
 void launch_scan(const double* S, int64_t ldS, int64_t n, int32_t validate_lower, uint8_t* subflag,
                  int32_t* bad, cudaStream_t st);
+// sharded S (extended local layout, sn_dist.h): flags of the columns this rank owns
+void launch_scan_dist(const double* Sx, int64_t ldx, int64_t n, int64_t P, int64_t bc, int64_t hc, int64_t rank,
+                      int32_t validate_lower, uint8_t* subflag, int32_t* bad, cudaStream_t st);
 void launch_window(const WindowArgs& a, cudaStream_t st);
 size_t window_smem_bytes();
 // kind: 0 = left update of S, 1 = right update of S, 2 = Q update; mt = 64/128/256

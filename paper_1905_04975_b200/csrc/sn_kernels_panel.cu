@@ -69,35 +69,47 @@ __global__ void __launch_bounds__(THREADS, 1) panel_kernel(PanelArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
 
-  // strip -> (window, index) by binary search over the level's prefix
-  const int sid = blockIdx.x;
-  int lo = 0, hi = a.nwin - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.prefix[mid] <= sid) lo = mid; else hi = mid - 1;
+  double* M = a.M;
+  int w, nx;       // window index within the level; valid columns (left) or rows (right/Q)
+  int64_t x0;      // first column (left) or row (right/Q) of the strip
+  if (a.strips) {
+    // explicit strip (sharded executor, sn_dist.h)
+    const StripDev sd = a.strips[blockIdx.x];
+    w = sd.w;
+    x0 = sd.x0;
+    nx = sd.cnt;
+  } else {
+    // strip -> (window, index) by binary search over the level's prefix
+    const int sid = blockIdx.x;
+    int lo = 0, hi = a.nwin - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.prefix[mid] <= sid) lo = mid; else hi = mid - 1;
+    }
+    w = lo;
+    const WinDev& wq = a.wins[w];
+    int strip = sid - a.prefix[w];
+    // critical strips (read by the next level's windows): a prefix of the left strips, a
+    // suffix of the right strips
+    if (KIND == 0 && a.part == 2) strip += wq.crit_l;
+    if (KIND == 1 && a.part == 1) strip += (int)((wq.j1 + NT - 1) / NT) - wq.crit_r;
+    if (C::LEFT) {
+      x0 = wq.j1 + wq.k + (int64_t)strip * NT;
+      nx = (int)min((int64_t)NT, a.n - x0);
+    } else {
+      x0 = (int64_t)strip * NT;
+      const int64_t lim = (KIND == 1) ? wq.j1 : a.n;
+      nx = (int)min((int64_t)NT, lim - x0);
+    }
   }
-  const int w = lo;
   if (a.status[a.base + w] == kWinSkipped) return;
   const WinDev wd = a.wins[w];
-  int strip = sid - a.prefix[w];
   const int k = wd.k;
   const int64_t j1 = wd.j1, ld = a.ld;
-  // critical strips (read by the next level's windows): a prefix of the left strips, a
-  // suffix of the right strips
-  if (KIND == 0 && a.part == 2) strip += wd.crit_l;
-  if (KIND == 1 && a.part == 1) strip += (int)((j1 + NT - 1) / NT) - wd.crit_r;
-  double* M = a.M;
+  // first column of the window's columns in M (right update: S may be stored with a column
+  // offset; Q and the left update's row index use the global index)
+  const int64_t jc = (KIND == 1) ? j1 + wd.coff : j1;
   const double* Z = a.Z + (int64_t)wd.slot * kZslot;
-  int64_t x0;      // first column (left) or row (right/Q) of the strip
-  int nx;          // valid columns/rows
-  if (C::LEFT) {
-    x0 = j1 + k + (int64_t)strip * NT;
-    nx = (int)min((int64_t)NT, a.n - x0);
-  } else {
-    x0 = (int64_t)strip * NT;
-    const int64_t lim = (KIND == 1) ? j1 : a.n;
-    nx = (int)min((int64_t)NT, lim - x0);
-  }
   const int nk = (k + KC - 1) / KC;
 
   auto load_stage = [&](int stage, int kc) {
@@ -123,7 +135,7 @@ __global__ void __launch_bounds__(THREADS, 1) panel_kernel(PanelArgs a) {
       for (int idx = tid; idx < NT * KC / 2; idx += kThreads) {
         const int kk = idx / (NT / 2), r = 2 * (idx % (NT / 2));
         const int nb = (kk0 + kk < k) ? 8 * max(0, min(2, nx - r)) : 0;
-        const double* src = nb ? M + (x0 + r) + (j1 + kk0 + kk) * ld : M;
+        const double* src = nb ? M + (x0 + r) + (jc + kk0 + kk) * ld : M;
         cp_async16z(Bs + kk * C::LDB + r, src, nb);
       }
     } else {
@@ -131,7 +143,7 @@ __global__ void __launch_bounds__(THREADS, 1) panel_kernel(PanelArgs a) {
       for (int idx = tid; idx < NT * KC; idx += kThreads) {
         const int kk = idx / NT, r = idx % NT;
         const bool v = (r < nx) && (kk0 + kk < k);
-        const double* src = v ? M + (x0 + r) + (j1 + kk0 + kk) * ld : M;
+        const double* src = v ? M + (x0 + r) + (jc + kk0 + kk) * ld : M;
         cp_async8(Bs + kk * C::LDB + r, src, v);
       }
     }
@@ -199,7 +211,7 @@ __global__ void __launch_bounds__(THREADS, 1) panel_kernel(PanelArgs a) {
           if (xx >= nx) continue;
           const double v = acc[i][j][2 * h + q];
           if (C::LEFT) M[(j1 + m) + (x0 + xx) * ld] = v;
-          else M[(x0 + xx) + (j1 + m) * ld] = v;
+          else M[(x0 + xx) + (jc + m) * ld] = v;
         }
       }
 }

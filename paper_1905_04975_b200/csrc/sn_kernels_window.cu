@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int widx = blockIdx.x;
   const WinDev wd = a.wins[widx];
-  const int sidx = a.base + widx;
+  const int sidx = wd.sidx;
   if (*(volatile int32_t*)&a.ctl->abort) {
     if (tid == 0) a.status[sidx] = kWinSkipped;
     return;
@@ -327,8 +327,8 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
   int64_t ioff = wd.pool + 2 * nb;
   ioff += ioff & 1;
   const uint16_t* inner = reinterpret_cast<const uint16_t*>(a.pool + ioff);
-  double* S = a.S;
   const int64_t ld = a.ldS;
+  double* S = a.S + wd.coff * ld;   // column j of S at column j + coff of the array
   const int64_t j1 = wd.j1;
   double* Z = a.Z + (int64_t)wd.slot * kZslot;
   // Z <- I (k x k, zero padded to 256 x 256)
