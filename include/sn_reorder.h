@@ -87,6 +87,9 @@ typedef struct sn_stats {
   double ms_kernel[5];       /* summed event time per kind (opts.profile = 1, else 0) */
   double flops_kernel[5];    /* algorithmic flops per kind (updates: 2 k^2 x panel extent) */
   double bytes_kernel[5];    /* algorithmic HBM bytes per kind (panel read + write once) */
+  double flops_exec_kernel[5]; /* flops the panel kernels execute: Z^T row groups skip the K
+                                  steps where Z is structurally zero; one-GPU
+                                  executor only, else 0 */
 } sn_stats;
 
 void sn_default_opts(sn_opts* o);

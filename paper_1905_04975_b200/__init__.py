@@ -61,11 +61,11 @@ class Stats(C.Structure):
                 ("eq_flops", C.c_double), ("ms_schedule", C.c_double), ("ms_device", C.c_double),
                 ("ms_total", C.c_double), ("ms_h2d", C.c_double), ("ms_d2h", C.c_double),
                 ("launches", C.c_int64 * 5), ("ms_kernel", C.c_double * 5), ("flops_kernel", C.c_double * 5),
-                ("bytes_kernel", C.c_double * 5)]
+                ("bytes_kernel", C.c_double * 5), ("flops_exec_kernel", C.c_double * 5)]
 
     def to_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}
-        for f in ("swaps_by_type", "launches", "ms_kernel", "flops_kernel", "bytes_kernel"):
+        for f in ("swaps_by_type", "launches", "ms_kernel", "flops_kernel", "bytes_kernel", "flops_exec_kernel"):
             d[f] = list(getattr(self, f))
         return d
 
@@ -246,8 +246,9 @@ def owned_columns(n: int, P: int, col_block: int, rank: int) -> np.ndarray:
 
 def shard(S, Q, P: int, col_block: int, rank: int):
     """Rank's shards of full S, Q (torch tensors holding the column-major matrices, as in
-    reorder()): S_loc (user_cols, n) and Q_loc (n, ceil(n/P)) tensors whose memory is the
-    column-major n x user_cols block columns and (q1-q0) x n row block (ld ceil(n/P))."""
+    reorder()): S_loc (user_cols, n) and Q_loc (n, ldq) tensors whose memory is the
+    column-major n x user_cols block columns and (q1-q0) x n row block (ldq = ceil(n/P)
+    rounded up to even, the same on every rank)."""
     import torch
     n = S.shape[0]
     uc, q0, q1 = dist_layout(n, P, col_block, rank)
@@ -258,7 +259,9 @@ def shard(S, Q, P: int, col_block: int, rank: int):
     Ql = None
     if Q is not None:
         # every rank's Q_loc has ld = ceil(n/P) (the last row block may be shorter)
-        Ql = torch.zeros((n, max(1, -(-n // P))), dtype=Q.dtype, device=Q.device)
+        qld = -(-n // P)
+        qld += qld & 1          # even: 16-byte aligned rows (TMA-describable)
+        Ql = torch.zeros((n, max(2, qld)), dtype=Q.dtype, device=Q.device)
         Ql[:, :q1 - q0] = Q[:, q0:q1]
     return Sl, Ql
 

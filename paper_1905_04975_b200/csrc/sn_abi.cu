@@ -48,7 +48,7 @@ struct DevBuf {
 };
 
 struct Workspace {
-  DevBuf wins, pool, prefix, status, ctl, Z, sub, bad;
+  DevBuf wins, pool, prefix, status, kwork, ctl, Z, zr, sub, bad;
   std::vector<cudaEvent_t> prof;   // event pool for opts.profile
   cudaStream_t sB = nullptr, sC = nullptr;
   cudaEvent_t evW[kZgen] = {}, evQ[kZgen] = {}, evCrit[kZgen] = {}, evRest[kZgen] = {};
@@ -330,8 +330,10 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   CK(ws.pool.ensure(P.pool.size() + 8));
   CK(ws.prefix.ensure(sizeof(int32_t) * pref.size()));
   CK(ws.status.ensure(sizeof(int32_t) * nw));
+  CK(ws.kwork.ensure(sizeof(int32_t) * nw));
   CK(ws.ctl.ensure(sizeof(Control)));
   CK(ws.Z.ensure(sizeof(double) * (size_t)kZslot * (size_t)(kZgen * maxper)));
+  CK(ws.zr.ensure(sizeof(int16_t) * (size_t)kZrange * (size_t)(kZgen * maxper)));
   CK(cudaMemcpyAsync(ws.wins.p, wd.data(), sizeof(WinDev) * nw, cudaMemcpyHostToDevice, sA));
   CK(cudaMemcpyAsync(ws.pool.p, P.pool.data(), P.pool.size(), cudaMemcpyHostToDevice, sA));
   CK(cudaMemcpyAsync(ws.prefix.p, pref.data(), sizeof(int32_t) * pref.size(), cudaMemcpyHostToDevice, sA));
@@ -347,6 +349,10 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   const bool overlapQ = o.q_stream_overlap != 0 && Q != nullptr;
   cudaStream_t sQ = overlapQ ? ws.sB : sA;
 
+  // TMA descriptors of S and Q (the cp.async kernels are used if TMA cannot describe them)
+  PanelMaps mapS{}, mapQ{};
+  panel_maps_init(&mapS, dZ, (int64_t)kZgen * maxper, S, n, n, ldS);
+  if (Q) panel_maps_init(&mapQ, dZ, (int64_t)kZgen * maxper, Q, n, n, ldQ);
   CK(cudaEventRecord(ws.ev0, sA));
   if (overlapQ) {
     CK(cudaStreamWaitEvent(ws.sB, ws.ev0, 0));
@@ -360,7 +366,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     WindowArgs wa{};
     wa.wins = dw + a; wa.nwin = (int32_t)cnt; wa.base = (int32_t)a;
     wa.pool = (const uint8_t*)ws.pool.p; wa.S = S; wa.ldS = ldS; wa.Z = dZ;
-    wa.status = dstatus; wa.ctl = dctl;
+    wa.status = dstatus; wa.ctl = dctl; wa.zrange = (int16_t*)ws.zr.p; wa.kwork = (int32_t*)ws.kwork.p;
     wa.force_order = o.force_reject_window; wa.force_swap = (int32_t)o.force_reject_swap;
     int pe = prof_begin(0, sA);
     launch_window(wa, sA);
@@ -371,8 +377,8 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     PanelArgs pa{};
     pa.strips = nullptr;
     pa.wins = dw + a; pa.nwin = (int32_t)cnt; pa.base = (int32_t)a; pa.status = dstatus;
-    pa.n = n; pa.Z = dZ;
-    pa.M = S; pa.ld = ldS;
+    pa.n = n; pa.Z = dZ; pa.zrange = (const int16_t*)ws.zr.p;
+    pa.M = S; pa.ld = ldS; pa.maps = &mapS;
     pa.vec16 = (ldS % 2 == 0 && ((uintptr_t)S % 16) == 0) ? 1 : 0;
     // the strips of the previous level's rest may overlap this level's strips
     if (look && l > 0) CK(cudaStreamWaitEvent(sA, ws.evRest[(l - 1) % kZgen], 0));
@@ -399,7 +405,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     }
     if (Q) {
       if (overlapQ) CK(cudaStreamWaitEvent(sQ, ws.evW[gen], 0));
-      pa.M = Q; pa.ld = ldQ;
+      pa.M = Q; pa.ld = ldQ; pa.maps = &mapQ;
       pa.vec16 = (ldQ % 2 == 0 && ((uintptr_t)Q % 16) == 0) ? 1 : 0;
       pa.prefix = dpref + pref_off[l * NK + 4];
       pa.part = 0;
@@ -443,7 +449,9 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   }
   final_blocks(P, sorted, ctl, ctl.abort ? status.data() : nullptr, n, bmap.data(), selrow.data(), fsz, fsel,
                &executed, &swaps, sbt);
-  double fk[5] = {0, 0, 0, 0, 0}, bk[5] = {0, 0, 0, 0, 0};
+  double fk[5] = {0, 0, 0, 0, 0}, bk[5] = {0, 0, 0, 0, 0}, fx[5] = {0, 0, 0, 0, 0};
+  std::vector<int32_t> kwork(nw, 0);
+  CK(cudaMemcpy(kwork.data(), ws.kwork.p, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < nw; ++i) {
     const WindowPlan& w = P.wins[sorted[i]];
     if (ctl.abort && status[i] == kWinSkipped) continue;
@@ -451,6 +459,8 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     const double eL = (double)(n - w.j1 - w.k), eR = (double)w.j1, eQ = Q ? (double)n : 0.0;
     eqf += k2 * (eL + eR + eQ);
     fk[1] += k2 * eL; fk[2] += k2 * eR; fk[3] += k2 * eQ;
+    const double kx = 256.0 * (double)kwork[i];   // executed flops per panel column / row
+    fx[1] += kx * eL; fx[2] += kx * eR; fx[3] += kx * eQ;
     bk[1] += 16.0 * kd * eL; bk[2] += 16.0 * kd * eR; bk[3] += 16.0 * kd * eQ;
     bk[0] += 16.0 * kd * kd + 8.0 * kZslot;
   }
@@ -485,6 +495,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
       st->ms_kernel[q] = mk[q];
       st->flops_kernel[q] = fk[q];
       st->bytes_kernel[q] = bk[q];
+      st->flops_exec_kernel[q] = fx[q];
     }
   }
   return ctl.abort ? SN_ERR_REJECTED : SN_OK;

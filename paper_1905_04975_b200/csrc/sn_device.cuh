@@ -1,12 +1,18 @@
 // sn_device.cuh -- device-side data layout shared by the executor and the kernels.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace sn {
 
 constexpr int kZld = 256;                 // Z slots are 256 x 256, column-major, ld 256
 constexpr int64_t kZslot = (int64_t)kZld * kZld;
+// Structure of Z: every column c of a window's accumulator is nonzero only in
+// the rows [lo[c], hi[c]] (an interval containing c: each swap mixes adjacent columns, so the
+// union of their intervals is again an interval).  Per Z slot, int16 lo[256] then hi[256];
+// columns >= k hold the empty interval (lo = 255, hi = 0).  Entries outside are exact zeros.
+constexpr int kZrange = 2 * kZld;
 constexpr int kInner = 64;                // max rows of an in-kernel inner window
 
 // One window, as seen by the kernels (sorted by level).
@@ -57,10 +63,22 @@ struct WindowArgs {
   double* S;
   int64_t ldS;
   double* Z;                // slot array base
+  int16_t* zrange;          // per slot: nonzero row interval of every Z column
   int32_t* status;          // indexed by sorted index
   Control* ctl;
+  int32_t* kwork;           // per sorted index: k4 steps the panel kernels execute per strip,
+                            // summed over the 32-row groups of Z^T (Z-structure skipping)
   int64_t force_order;      // debug: schedule order of the window to reject in (-1 none)
   int32_t force_swap;       // debug: swap index (execution order) to reject
+};
+
+// TMA descriptors of one panel launch target (host side; passed to the kernels by value as
+// __grid_constant__ parameters): the Z slot array for MT = 64/128/256 and the matrix M (S or Q)
+// for the left (K rows x 64 columns) and right/Q (68 rows x 16 K columns) boxes.
+struct PanelMaps {
+  CUtensorMap z[3];
+  CUtensorMap mL, mRQ;
+  int valid;
 };
 
 struct PanelArgs {
@@ -76,6 +94,8 @@ struct PanelArgs {
   int64_t ld;
   int64_t n;
   const double* Z;
+  const int16_t* zrange;    // per slot row intervals of Z's columns (window kernel output)
+  const PanelMaps* maps;    // host pointer: TMA descriptors (NULL or !valid: cp.async kernel)
 };
 
 // kernel launchers (sn_kernels_*.cu)
@@ -89,5 +109,9 @@ size_t window_smem_bytes();
 // kind: 0 = left update of S, 1 = right update of S, 2 = Q update; mt = 64/128/256
 void launch_panel(int kind, int mt, const PanelArgs& a, int32_t nstrips, cudaStream_t st);
 int panel_strip_width(int kind, int mt);
+// TMA path (sn_kernels_panel_tma.cu)
+bool panel_maps_init(PanelMaps* pm, const double* Zbase, int64_t nslots, const double* M, int64_t rows, int64_t cols,
+                     int64_t ld);
+void launch_panel_tma(int kind, int mt, const PanelArgs& a, int32_t nstrips, const PanelMaps& pm, cudaStream_t st);
 
 }  // namespace sn

@@ -128,7 +128,7 @@ struct DBuf {
 };
 
 struct DistWorkspace {
-  DBuf wins, pool, status, ctl, Z, sub, bad;
+  DBuf wins, pool, status, ctl, Z, zr, sub, bad;
   std::vector<DBuf> Sx, own, strips, stage;   // per local rank
   cudaStream_t sB = nullptr;
   cudaEvent_t evW[kZgenD] = {}, evQ[kZgenD] = {};
@@ -345,6 +345,8 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
     DCK(ws.Z.ensure(zbytes));
     DCK(cudaMemsetAsync(ws.Z.p, 0, zbytes, sA));
   }
+  DCK(ws.zr.ensure(sizeof(int16_t) * (size_t)kZrange * (size_t)(kZgenD * maxper)));
+  int16_t* dzr = (int16_t*)ws.zr.p;
   DCK(cudaMemcpyAsync(ws.wins.p, wd.data(), sizeof(WinDev) * nw, cudaMemcpyHostToDevice, sA));
   DCK(cudaMemcpyAsync(ws.pool.p, plan.pool.data(), plan.pool.size(), cudaMemcpyHostToDevice, sA));
   DCK(cudaMemsetAsync(ws.status.p, 0, sizeof(int32_t) * nw, sA));
@@ -373,6 +375,15 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
   double* dZ = (double*)ws.Z.p;
   const bool overlapQ = o.q_stream_overlap != 0 && hasQ;
   cudaStream_t sQ = overlapQ ? ws.sB : sA;
+  std::vector<PanelMaps> mapS(nloc), mapQ(nloc);
+  for (int64_t q = 0; q < nloc; ++q) {
+    const int64_t r = rr[q].rank;
+    std::memset(&mapS[q], 0, sizeof(PanelMaps));
+    std::memset(&mapQ[q], 0, sizeof(PanelMaps));
+    if (lay.ext_cols(r) > 0) panel_maps_init(&mapS[q], dZ, (int64_t)kZgenD * maxper, rr[q].Sx, n, lay.ext_cols(r), ldx);
+    if (hasQ && lay.q1(r) > lay.q0(r))
+      panel_maps_init(&mapQ[q], dZ, (int64_t)kZgenD * maxper, io[q].Q, lay.q1(r) - lay.q0(r), n, ldq);
+  }
   DCK(cudaEventRecord(ws.ev0, sA));
   if (overlapQ) DCK(cudaStreamWaitEvent(ws.sB, ws.ev0, 0));
 
@@ -391,7 +402,7 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
       WindowArgs wa{};
       wa.wins = R.d_own + a; wa.nwin = (int32_t)c; wa.base = 0;
       wa.pool = (const uint8_t*)ws.pool.p; wa.S = R.Sx; wa.ldS = ldx; wa.Z = dZ;
-      wa.status = dstatus; wa.ctl = dctl;
+      wa.status = dstatus; wa.ctl = dctl; wa.zrange = dzr;
       wa.force_order = o.force_reject_window; wa.force_swap = (int32_t)o.force_reject_swap;
       launch_window(wa, sA);
       launches[0]++;
@@ -403,6 +414,8 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
       for (int64_t i = w0; i < w0 + cnt; ++i) {
         double* z = dZ + (int64_t)wd[i].slot * kZslot;
         NCK(g_nccl.Broadcast(z, z, (size_t)wd[i].k * kZld, ncclFloat64, G.wins[i].owner, g_comm.comm, sA));
+        int16_t* zr = dzr + (int64_t)wd[i].slot * kZrange;
+        NCK(g_nccl.Broadcast(zr, zr, (size_t)kZrange * 2, ncclUint8, G.wins[i].owner, g_comm.comm, sA));
       }
       NCK(g_nccl.AllReduce(dstatus + w0, dstatus + w0, (size_t)cnt, ncclInt32, ncclMax, g_comm.comm, sA));
       NCK(g_nccl.AllReduce(&dctl->abort, &dctl->abort, 1, ncclInt32, ncclMax, g_comm.comm, sA));
@@ -419,7 +432,7 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
         PanelArgs pa{};
         pa.wins = dw + w0; pa.nwin = (int32_t)cnt; pa.base = (int32_t)w0; pa.status = dstatus;
         pa.strips = R.d_strips + s0; pa.prefix = nullptr; pa.part = 0;
-        pa.n = n; pa.Z = dZ; pa.M = R.Sx; pa.ld = ldx;
+        pa.n = n; pa.Z = dZ; pa.zrange = dzr; pa.M = R.Sx; pa.ld = ldx; pa.maps = &mapS[q];
         pa.vec16 = ((uintptr_t)R.Sx % 16) == 0 ? 1 : 0;
         launch_panel(kind, mt, pa, (int32_t)(s1 - s0), sA);
         launches[1 + kind]++;
@@ -438,7 +451,8 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
         PanelArgs pa{};
         pa.wins = dw + w0; pa.nwin = (int32_t)cnt; pa.base = (int32_t)w0; pa.status = dstatus;
         pa.strips = R.d_strips + LR.Q0; pa.prefix = nullptr; pa.part = 0;
-        pa.n = lay.q1(R.rank) - lay.q0(R.rank); pa.Z = dZ; pa.M = io[q].Q; pa.ld = ldq;
+        pa.n = lay.q1(R.rank) - lay.q0(R.rank); pa.Z = dZ; pa.zrange = dzr; pa.M = io[q].Q; pa.ld = ldq;
+        pa.maps = &mapQ[q];
         pa.vec16 = (ldq % 2 == 0 && ((uintptr_t)io[q].Q % 16) == 0) ? 1 : 0;
         launch_panel(2, mt, pa, (int32_t)(LR.Q1 - LR.Q0), sQ);
         launches[3]++;

@@ -111,6 +111,18 @@ __global__ void __launch_bounds__(THREADS, 1) panel_kernel(PanelArgs a) {
   const int64_t jc = (KIND == 1) ? j1 + wd.coff : j1;
   const double* Z = a.Z + (int64_t)wd.slot * kZslot;
   const int nk = (k + KC - 1) / KC;
+  // Z structure: output rows m of a 16-row tile only need the K rows where
+  // one of the tile's Z columns is nonzero; outside that interval the DMMAs (and the A
+  // loads) are skipped.  The skipped products are exact zeros, so results are unchanged.
+  __shared__ int16_t s_tlo[MT / 16], s_thi[MT / 16];
+  if (tid < MT / 16) {
+    const int16_t* zr = a.zrange + (int64_t)wd.slot * kZrange;
+    int lo = kZld, hi = -1;
+    for (int c = 16 * tid; c < 16 * tid + 16; ++c) { lo = min(lo, (int)zr[c]); hi = max(hi, (int)zr[kZld + c]); }
+    s_tlo[tid] = (int16_t)lo;
+    s_thi[tid] = (int16_t)hi;
+  }
+  __syncthreads();
 
   auto load_stage = [&](int stage, int kc) {
     double* As = smem + stage * C::STAGE;
@@ -159,6 +171,13 @@ __global__ void __launch_bounds__(THREADS, 1) panel_kernel(PanelArgs a) {
 
   const int wm0 = (warp % C::WM) * (MT / C::WM);
   const int wn0 = (warp / C::WM) * (NT / C::WN);
+  // K interval of this warp's output rows (warp-uniform: the skip is one branch per k4 step)
+  int wlo = kZld, whi = -1;
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i) {
+    wlo = min(wlo, (int)s_tlo[(wm0 >> 4) + i]);
+    whi = max(whi, (int)s_thi[(wm0 >> 4) + i]);
+  }
 
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
@@ -177,6 +196,8 @@ __global__ void __launch_bounds__(THREADS, 1) panel_kernel(PanelArgs a) {
     // MI*NI-1 independent ones (the m16n8k8 form chains two 8x8x4 DMMAs back to back).
 #pragma unroll
     for (int ks = 0; ks < KC; ks += 4) {
+      const int kg = kc * KC + ks;
+      if (kg + 3 < wlo || kg > whi) continue;   // Z^T rows of this warp are exact zeros here
       double a0[C::MI], a1[C::MI], bf[C::NI];
 #pragma unroll
       for (int i = 0; i < C::MI; ++i) {
@@ -246,6 +267,10 @@ int panel_strip_width(int kind, int mt) { (void)kind; (void)mt; return 64; }
 
 void launch_panel(int kind, int mt, const PanelArgs& a, int32_t nstrips, cudaStream_t st) {
   if (nstrips <= 0) return;
+  if (a.maps && a.maps->valid) {
+    launch_panel_tma(kind, mt, a, nstrips, *a.maps, st);
+    return;
+  }
   if (kind == 0) launch_kind<0>(mt, a, nstrips, st);
   else if (kind == 1) launch_kind<1>(mt, a, nstrips, st);
   else launch_kind<2>(mt, a, nstrips, st);

@@ -25,6 +25,8 @@ constexpr int LDT = 68;   // staging tile
 // block list of the window being processed (one CTA per window)
 __shared__ uint8_t g_bsz[256], g_bsel[256];
 __shared__ int16_t g_brow[257];
+// nonzero row interval of every column of the outer accumulator Z (sn_device.cuh kZrange)
+__shared__ int16_t g_zlo[256], g_zhi[256];
 
 __device__ __forceinline__ void mma_16x8x8(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
   asm volatile(
@@ -252,6 +254,18 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
       const int j = W.lj[buf][ty][sl];
       dev::swap_apply_cols_t(ty, Din, LDD, j, j, rec[ty][sl], lane);
       dev::swap_apply_cols_t(ty, Zin, LDZ, kin, j, rec[ty][sl], lane);
+      {
+        // the swap mixes outer Z columns i1+j .. i1+j+n1+n2-1 (concurrent swaps: disjoint);
+        // lanes 0..3 hold one column each, reduced over groups of 4 lanes
+        const int c = i1 + j + (lane & 3), nc = (ty >> 1) + (ty & 1) + 2;
+        const bool mine = (lane & 3) < nc;
+        int lo = mine ? g_zlo[c] : kZld, hi = mine ? g_zhi[c] : -1;
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
+        if (lane < 4 && mine) { g_zlo[c] = (int16_t)lo; g_zhi[c] = (int16_t)hi; }
+      }
     }
     const bool stop = W.anyrej != 0;
     if (warp == 0 && !stop && t + 1 < T) wave_prepare(W, t + 1, lane);
@@ -324,6 +338,10 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
   const int k = wd.k, nb = wd.nblk;
   const uint8_t* pool = a.pool + wd.pool;
   for (int b = tid; b < nb; b += kThreads) { bsz[b] = pool[b]; bsel[b] = pool[nb + b]; }
+  for (int c = tid; c < kZld; c += kThreads) {
+    g_zlo[c] = (int16_t)(c < wd.k ? c : kZld - 1);
+    g_zhi[c] = (int16_t)(c < wd.k ? c : 0);
+  }
   int64_t ioff = wd.pool + 2 * nb;
   ioff += ioff & 1;
   const uint16_t* inner = reinterpret_cast<const uint16_t*>(a.pool + ioff);
@@ -371,6 +389,29 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
     inner_update<false>(Z, kZld, 0, i1, k, kin, Zin, Tb, tid);                   // Z columns
     __syncthreads();
     if (W.anyrej) break;
+  }
+  {
+    int16_t* zr = a.zrange + (int64_t)wd.slot * kZrange;
+    for (int c = tid; c < kZld; c += kThreads) { zr[c] = g_zlo[c]; zr[kZld + c] = g_zhi[c]; }
+    // executed work of the panel kernels for this Z: per 32-row group of Z^T rows (a warp's M
+    // rows), the k4 steps of [0, 16*ceil(k/16)) that meet the group's K interval
+    if (warp == 0 && a.kwork) {
+      int total = 0;
+      const int kpad = 16 * ((k + 15) / 16);
+      for (int g0 = 0; g0 < kZld; g0 += 32) {
+        int lo = g_zlo[g0 + lane], hi = g_zhi[g0 + lane];
+        for (int o = 16; o > 0; o >>= 1) {
+          lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+          hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (g0 < k && hi >= lo) {
+          int cnt = 0;
+          for (int kg = 0; kg < kpad; kg += 4) cnt += (kg + 3 >= lo && kg <= hi) ? 1 : 0;
+          total += cnt;
+        }
+      }
+      if (lane == 0) a.kwork[sidx] = total;
+    }
   }
   if (tid == 0) {
     if (W.anyrej) {
