@@ -406,6 +406,8 @@ def main():
                          "launches": launches_dom, "traffic": traffic, "traffic_note": traffic_note},
             "kernel_share": share,
             "kernel_share_isolated": iso_share,
+            "isolated_step_ms": iso_ms,
+            "kernel_ms_isolated": {kinds[q]: msi[q] for q in range(5)},
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": gpu_launches,

@@ -353,6 +353,11 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   PanelMaps mapS{}, mapQ{};
   panel_maps_init(&mapS, dZ, (int64_t)kZgen * maxper, S, n, n, ldS);
   if (Q) panel_maps_init(&mapQ, dZ, (int64_t)kZgen * maxper, Q, n, n, ldQ);
+  unsigned long long* dtp = nullptr;   // SN_WPROF: window-kernel phase cycles (debug)
+  if (std::getenv("SN_WPROF")) {
+    CK(cudaMalloc(&dtp, 16 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(dtp, 0, 16 * sizeof(unsigned long long), sA));
+  }
   CK(cudaEventRecord(ws.ev0, sA));
   if (overlapQ) {
     CK(cudaStreamWaitEvent(ws.sB, ws.ev0, 0));
@@ -367,6 +372,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     wa.wins = dw + a; wa.nwin = (int32_t)cnt; wa.base = (int32_t)a;
     wa.pool = (const uint8_t*)ws.pool.p; wa.S = S; wa.ldS = ldS; wa.Z = dZ;
     wa.status = dstatus; wa.ctl = dctl; wa.zrange = (int16_t*)ws.zr.p; wa.kwork = (int32_t*)ws.kwork.p;
+    wa.tprof = dtp;
     wa.force_order = o.force_reject_window; wa.force_swap = (int32_t)o.force_reject_swap;
     int pe = prof_begin(0, sA);
     launch_window(wa, sA);
@@ -436,6 +442,18 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   CK(cudaStreamSynchronize(sA));
   float dev_ms = 0.f;
   CK(cudaEventElapsedTime(&dev_ms, ws.ev0, ws.ev1));
+  if (dtp) {
+    unsigned long long h[16];
+    CK(cudaMemcpy(h, dtp, sizeof(h), cudaMemcpyDeviceToHost));
+    cudaFree(dtp);
+    const double nwin = (double)(h[9] ? h[9] : 1);
+    std::fprintf(stderr,
+                 "{\"probe\":\"window_phases\",\"windows\":%llu,\"steps_per_window\":%.1f,\"cycles_per_window\":"
+                 "{\"A\":%.0f,\"B\":%.0f,\"C\":%.0f,\"wave_setup\":%.0f,\"staging\":%.0f,\"inner_updates\":%.0f,"
+                 "\"total\":%.0f,\"B_work_avg_warp\":%.0f,\"B_work_max_warp\":%.0f,\"A_transform_max\":%.0f}}\n",
+                 h[9], h[4] / nwin, h[0] / nwin, h[1] / nwin, h[2] / nwin, h[5] / nwin, h[6] / nwin, h[7] / nwin,
+                 h[8] / nwin, h[10] / nwin / 8.0, h[11] / nwin, h[12] / nwin);
+  }
 
   // ---- outputs: final block list
   std::vector<uint8_t> fsz, fsel;

@@ -66,6 +66,7 @@ struct WindowArgs {
   int16_t* zrange;          // per slot: nonzero row interval of every Z column
   int32_t* status;          // indexed by sorted index
   Control* ctl;
+  unsigned long long* tprof;  // debug: per-phase cycle counters (NULL: off)
   int32_t* kwork;           // per sorted index: k4 steps the panel kernels execute per strip,
                             // summed over the 32-row groups of Z^T (Z-structure skipping)
   int64_t force_order;      // debug: schedule order of the window to reject in (-1 none)

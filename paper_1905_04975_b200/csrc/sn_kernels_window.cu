@@ -10,6 +10,7 @@
 // level-3 update, one level down.  The outer Z is left in a 256x256 slot for
 // the panel kernels.
 #include <cstdint>
+#include <cstdlib>
 
 #include "sn_device.cuh"
 #include "sn_swap.cuh"
@@ -21,6 +22,8 @@ constexpr int kThreads = 256;
 constexpr int LDD = 65;   // inner window (odd stride: conflict-free row walks)
 constexpr int LDZ = 68;   // inner accumulator (== 4 mod 16: conflict-free DMMA fragments)
 constexpr int LDT = 68;   // staging tile
+
+__device__ int g_wdbg;   // debug: 1 skip phase B, 2 skip phase C (timing experiments only)
 
 // block list of the window being processed (one CTA per window)
 __shared__ uint8_t g_bsz[256], g_bsel[256];
@@ -141,6 +144,8 @@ struct WaveShared {
   int cnt[2][4], nflat[2];
   int8_t frej[64];
   int anyrej, done, laststep;
+  int8_t zlo[64], zhi[64];            // nonzero row interval of every column of Zin
+  unsigned long long bmax, bmax_sum, amax, amax_sum;  // debug timing (tprof)
   int rej_row, rej_n1, rej_n2;
 };
 
@@ -177,9 +182,13 @@ __device__ void wave_prepare(WaveShared& W, int t, int lane) {
   if (lane == 0) W.nflat[buf] = __popc(amask);
 }
 
+// debug timing (WindowArgs::tprof): cycles of tid 0 per phase, summed over windows
+// [0] A transforms, [1] B rows, [2] C columns, [3] step tail, [4] steps, [5] wave setup,
+// [6] staging, [7] write-back + inner updates, [8] kernel total, [9] windows
 __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Din, double* Zin,
                                 WaveShared& W, int tid, int warp, int lane, bool force_here, int force_swap,
-                                int done_before) {
+                                int done_before, unsigned long long* tp) {
+  long long c0 = tp && tid == 0 ? clock64() : 0, cA = 0, cB = 0, cC = 0, cT = 0, cS = 0, cBw = 0;
   __shared__ double rec[4][32][dev::kRec];
   if (tid == 0) {
     // movers / unselected lists of the inner window (block list in s_bsz/s_bsel)
@@ -203,9 +212,12 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
     W.anyrej = 0; W.laststep = -1;
     W.done = done_before;
   }
+  if (tid < kInner) { W.zlo[tid] = (int8_t)tid; W.zhi[tid] = (int8_t)tid; }
+  if (tid == 0) { W.bmax = 0; W.bmax_sum = 0; W.amax = 0; W.amax_sum = 0; }
   __syncthreads();
   if (warp == 0) wave_prepare(W, 0, lane);
   __syncthreads();
+  if (tp && tid == 0) { const long long c = clock64(); cS = c - c0; c0 = c; }
   const int T = W.T;
   int t = 0;
   for (; t < T; ++t) {
@@ -216,9 +228,15 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
       const int j = W.lj[buf][warp][lane];
       const int flat = W.lflat[buf][warp][lane];
       bool rj = force_here && (base + flat == force_swap);
+      const long long ta = tp ? clock64() : 0;
       if (!rj) rj = dev::swap_compute_t(warp, Din, LDD, j, rec[warp][lane]);
+      if (tp) atomicMax(&W.amax, (unsigned long long)(clock64() - ta));
       W.frej[flat] = rj ? 1 : 0;
       if (rj) atomicOr(&W.anyrej, 1);
+    } else if (warp == kThreads / 32 - 1) {
+      // the last warp (idle in phase A) prepares the next step's swap lists (double-buffered
+      // by step parity; they depend only on the inner window's static mover/unselected lists)
+      if (t + 1 < T) wave_prepare(W, t + 1, lane);
     } else if (warp == 3) {
       const int c3 = W.cnt[buf][3];
       for (int b0 = 0; b0 < c3; b0 += 16) {
@@ -227,7 +245,9 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
         const int sl = act ? slot : b0;
         const int j = W.lj[buf][3][sl];
         double tmp[dev::kRec];
+        const long long ta = tp ? clock64() : 0;
         bool rj = dev::swap_compute_22_paired(Din, LDD, j, tmp, role);
+        if (tp) atomicMax(&W.amax, (unsigned long long)(clock64() - ta));
         if (act && role == 0) {
           const int flat = W.lflat[buf][3][slot];
           rj = rj || (force_here && (base + flat == force_swap));
@@ -239,21 +259,38 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
       }
     }
     __syncthreads();
+    if (tp && tid == 0) { const long long c = clock64(); cA += c - c0; c0 = c; }
     const int nf = W.nflat[buf];
     // B: rows
-    for (int f = warp; f < nf; f += kThreads / 32) {
+    const long long cb0 = tp && lane == 0 ? clock64() : 0;
+    for (int f = warp; f < ((g_wdbg & 1) ? 0 : nf); f += kThreads / 32) {
       if (W.frej[f]) continue;
       const int ty = W.ftype[buf][f], sl = W.fslot[buf][f];
       dev::swap_apply_rows_t(ty, Din, LDD, kin, W.lj[buf][ty][sl], rec[ty][sl], lane);
     }
+    if (tp && lane == 0) {
+      const long long d = clock64() - cb0;
+      cBw += d;
+      atomicMax(&W.bmax, (unsigned long long)d);
+    }
     __syncthreads();
+    if (tp && tid == 0) { const long long c = clock64(); cB += c - c0; c0 = c; }
     // C: columns of the window and of the accumulator
-    for (int f = warp; f < nf; f += kThreads / 32) {
+    for (int f = warp; f < ((g_wdbg & 2) ? 0 : nf); f += kThreads / 32) {
       if (W.frej[f]) continue;
       const int ty = W.ftype[buf][f], sl = W.fslot[buf][f];
       const int j = W.lj[buf][ty][sl];
       dev::swap_apply_cols_t(ty, Din, LDD, j, j, rec[ty][sl], lane);
-      dev::swap_apply_cols_t(ty, Zin, LDZ, kin, j, rec[ty][sl], lane);
+      {
+        // Zin columns j..j+nd-1 are zero outside the union of their row intervals (Zin starts
+        // as I and every swap mixes adjacent columns): apply the transform there only
+        const int nd = (ty >> 1) + (ty & 1) + 2;
+        int lo = W.zlo[j], hi = W.zhi[j];
+        for (int c = 1; c < nd; ++c) { lo = min(lo, (int)W.zlo[j + c]); hi = max(hi, (int)W.zhi[j + c]); }
+        dev::swap_apply_cols_t(ty, Zin + lo, LDZ, hi - lo + 1, j, rec[ty][sl], lane);
+        __syncwarp();
+        if (lane < nd) { W.zlo[j + lane] = (int8_t)lo; W.zhi[j + lane] = (int8_t)hi; }
+      }
       {
         // the swap mixes outer Z columns i1+j .. i1+j+n1+n2-1 (concurrent swaps: disjoint);
         // lanes 0..3 hold one column each, reduced over groups of 4 lanes
@@ -268,23 +305,46 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
       }
     }
     const bool stop = W.anyrej != 0;
-    if (warp == 0 && !stop && t + 1 < T) wave_prepare(W, t + 1, lane);
-    __syncthreads();
-    if (tid == 0) {
-      int nrej = 0, first = -1;
-      for (int f = 0; f < nf; ++f)
-        if (W.frej[f]) { ++nrej; if (first < 0) first = f; }
-      W.done += nf - nrej;
-      if (first >= 0) {
-        const int ty = W.ftype[buf][first], sl = W.fslot[buf][first];
-        W.rej_row = i1 + W.lj[buf][ty][sl];   // window-local row
-        W.rej_n1 = (ty >> 1) + 1;
-        W.rej_n2 = (ty & 1) + 1;
-      }
+    if (tid == 0 && !stop) {
+      // common case (nothing rejected): the step's bookkeeping, no extra barrier
+      W.done = base + nf;
       W.laststep = t;
     }
     __syncthreads();
-    if (stop) break;
+    if (tp && tid == 0) {
+      const long long c = clock64(); cC += c - c0; c0 = c;
+      W.bmax_sum += W.bmax;
+      W.bmax = 0;
+      W.amax_sum += W.amax;
+      W.amax = 0;
+    }
+    if (stop) {
+      if (tid == 0) {
+        int nrej = 0, first = -1;
+        for (int f = 0; f < nf; ++f)
+          if (W.frej[f]) { ++nrej; if (first < 0) first = f; }
+        W.done += nf - nrej;
+        if (first >= 0) {
+          const int ty = W.ftype[buf][first], sl = W.fslot[buf][first];
+          W.rej_row = i1 + W.lj[buf][ty][sl];   // window-local row
+          W.rej_n1 = (ty >> 1) + 1;
+          W.rej_n2 = (ty & 1) + 1;
+        }
+        W.laststep = t;
+      }
+      __syncthreads();
+      break;
+    }
+  }
+  if (tp && tid == 0) {
+    atomicAdd(&tp[0], (unsigned long long)cA); atomicAdd(&tp[1], (unsigned long long)cB);
+    atomicAdd(&tp[2], (unsigned long long)cC); atomicAdd(&tp[3], (unsigned long long)cT);
+    atomicAdd(&tp[4], (unsigned long long)t); atomicAdd(&tp[5], (unsigned long long)cS);
+  }
+  if (tp && lane == 0) {
+    atomicAdd(&tp[10], (unsigned long long)cBw);   // summed over the 8 warps
+    if (tid == 0) atomicAdd(&tp[11], W.bmax_sum);   // per step max over warps, summed
+    if (tid == 0) atomicAdd(&tp[12], W.amax_sum);   // per step max transform latency, summed
   }
   // new block arrangement of [top, bottom)
   if (tid == 0) {
@@ -364,6 +424,8 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
   __syncthreads();
 
   int swaps_done = 0;
+  long long ck = clock64();
+  const long long ck0 = ck;
   for (int q = 0; q < wd.ninner; ++q) {
     const int top = inner[2 * q], bottom = inner[2 * q + 1];
     const int i1 = brow[top], i2 = brow[bottom];
@@ -375,8 +437,10 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
       Zin[r + c * LDZ] = (r == c && r < kin) ? 1.0 : 0.0;
     }
     __syncthreads();
+    if (a.tprof && tid == 0) { const long long c = clock64(); atomicAdd(&a.tprof[6], (unsigned long long)(c - ck)); ck = c; }
     wavefront_swaps(top, bottom, i1, kin, Din, Zin, W, tid, warp, lane, wd.order == a.force_order,
-                    a.force_swap, swaps_done);
+                    a.force_swap, swaps_done, a.tprof);
+    if (a.tprof && tid == 0) ck = clock64();
     swaps_done = W.done;
     // write the inner window back
     for (int idx = tid; idx < kInner * kInner; idx += kThreads) {
@@ -388,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
     inner_update<true>(S, ld, j1 + i1, j1 + i2, k - i2, kin, Zin, Tb, tid);      // cols right
     inner_update<false>(Z, kZld, 0, i1, k, kin, Zin, Tb, tid);                   // Z columns
     __syncthreads();
+    if (a.tprof && tid == 0) { const long long c = clock64(); atomicAdd(&a.tprof[7], (unsigned long long)(c - ck)); ck = c; }
     if (W.anyrej) break;
   }
   {
@@ -413,6 +478,10 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
       if (lane == 0) a.kwork[sidx] = total;
     }
   }
+  if (a.tprof && tid == 0) {
+    atomicAdd(&a.tprof[8], (unsigned long long)(clock64() - ck0));
+    atomicAdd(&a.tprof[9], 1ull);
+  }
   if (tid == 0) {
     if (W.anyrej) {
       a.ctl->abort = 1;
@@ -437,6 +506,13 @@ size_t window_smem_bytes() {
 
 void launch_window(const WindowArgs& a, cudaStream_t st) {
   static bool attr = false;
+  static const int wdbg = [] {
+    const char* e = std::getenv("SN_WDBG");
+    const int v = e ? std::atoi(e) : 0;
+    cudaMemcpyToSymbol(g_wdbg, &v, sizeof(int));
+    return v;
+  }();
+  (void)wdbg;
   const size_t smem = window_smem_bytes();
   if (!attr) {
     cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
