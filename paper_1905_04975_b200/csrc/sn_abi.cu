@@ -50,7 +50,8 @@ struct DevBuf {
 struct Workspace {
   DevBuf wins, pool, prefix, status, kwork, ctl, Z, zr, sub, bad;
   std::vector<cudaEvent_t> prof;   // event pool for opts.profile
-  cudaStream_t sB = nullptr, sC = nullptr;
+  cudaStream_t sB = nullptr, sC = nullptr, sU = nullptr;   // sU: host->device upload of Q
+  cudaEvent_t evQup = nullptr;
   cudaEvent_t evW[kZgen] = {}, evQ[kZgen] = {}, evCrit[kZgen] = {}, evRest[kZgen] = {};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evJoin = nullptr, evJoinC = nullptr;
   int device = -1;
@@ -77,7 +78,7 @@ double now_ms() {
     }                                                                  \
   } while (0)
 
-static int ensure_runtime(Workspace& ws) {
+int ensure_runtime(Workspace& ws) {
   int dev = 0;
   CK(cudaGetDevice(&dev));
   if (ws.device != dev) {
@@ -93,6 +94,8 @@ static int ensure_runtime(Workspace& ws) {
     }
     CK(cudaStreamCreateWithFlags(&ws.sB, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&ws.sC, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ws.sU, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ws.evQup, cudaEventDisableTiming));
     for (int i = 0; i < kZgen; ++i) {
       CK(cudaEventCreateWithFlags(&ws.evW[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&ws.evQ[i], cudaEventDisableTiming));
@@ -205,8 +208,10 @@ void write_blocks(const std::vector<uint8_t>& fsz, const std::vector<uint8_t>& f
 
 namespace {
 
+// q_ready (optional): an event after which Q holds its input (a host upload still in flight
+// while the structure scan, the plan and the first levels' S updates run)
 int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ, int32_t* select,
-        int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA) {
+        int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA, cudaEvent_t q_ready = nullptr) {
   Workspace& ws = g_ws;
   const double t_start = now_ms();
   if (int rc = ensure_runtime(ws)) return rc;
@@ -312,6 +317,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   const double t_plan = now_ms();
 
   if (nw == 0) {
+    if (q_ready) CK(cudaStreamWaitEvent(sA, q_ready, 0));
     if (bmap_out) std::memcpy(bmap_out, bmap.data(), (size_t)n);
     if (st) {
       std::memset(st, 0, sizeof(*st));
@@ -410,6 +416,7 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
       CK(cudaGetLastError());
     }
     if (Q) {
+      if (l == 0 && q_ready) CK(cudaStreamWaitEvent(sQ, q_ready, 0));
       if (overlapQ) CK(cudaStreamWaitEvent(sQ, ws.evW[gen], 0));
       pa.M = Q; pa.ld = ldQ; pa.maps = &mapQ;
       pa.vec16 = (ldQ % 2 == 0 && ((uintptr_t)Q % 16) == 0) ? 1 : 0;
@@ -582,23 +589,33 @@ int sn_reorder_schur_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS, 
   const bool devQ = Q == nullptr || sn::is_device_ptr(Q);
   if (devS != devQ) return -4;
   if (devS) return sn::run(o, n, S, ldS, Q, ldQ, select, m, bmap_out, stats, sA);
-  // host buffers: stage through device memory (the copies are part of the call)
+  // host buffers: stage through device memory (the copies are part of the call).  S goes up
+  // first (the scan and the plan need it); Q goes up on its own stream while the structure
+  // scan, the plan and the first levels' S work run -- the Q updates wait for it.
   const double t0 = sn::now_ms();
+  if (int rc = sn::ensure_runtime(sn::g_ws)) return rc;
   double *dS = nullptr, *dQ = nullptr;
   const size_t bytes = sizeof(double) * (size_t)n * (size_t)n;
   if (cudaMalloc(&dS, bytes) != cudaSuccess) return SN_ERR_CUDA;
   if (Q && cudaMalloc(&dQ, bytes) != cudaSuccess) { cudaFree(dS); return SN_ERR_CUDA; }
+  auto copy = [&](double* dst, int64_t ldd, const double* src, int64_t lds, cudaMemcpyKind kind, cudaStream_t s) {
+    if (ldd == n && lds == n) return cudaMemcpyAsync(dst, src, bytes, kind, s);   // one contiguous copy
+    return cudaMemcpy2DAsync(dst, ldd * 8, src, lds * 8, n * 8, n, kind, s);
+  };
+  cudaStream_t sU = sn::g_ws.sU;
   int rc = SN_OK;
-  if (cudaMemcpy2DAsync(dS, n * 8, S, ldS * 8, n * 8, n, cudaMemcpyHostToDevice, sA) != cudaSuccess ||
-      (Q && cudaMemcpy2DAsync(dQ, n * 8, Q, ldQ * 8, n * 8, n, cudaMemcpyHostToDevice, sA) != cudaSuccess) ||
-      cudaStreamSynchronize(sA) != cudaSuccess)
+  if (copy(dS, n, S, ldS, cudaMemcpyHostToDevice, sA) != cudaSuccess) rc = SN_ERR_CUDA;
+  if (rc == SN_OK && Q &&
+      (copy(dQ, n, Q, ldQ, cudaMemcpyHostToDevice, sU) != cudaSuccess ||
+       cudaEventRecord(sn::g_ws.evQup, sU) != cudaSuccess))
     rc = SN_ERR_CUDA;
   const double t1 = sn::now_ms();
-  if (rc == SN_OK) rc = sn::run(o, n, dS, n, dQ, n, select, m, bmap_out, stats, sA);
+  if (rc == SN_OK) rc = sn::run(o, n, dS, n, dQ, n, select, m, bmap_out, stats, sA, Q ? sn::g_ws.evQup : nullptr);
+  if (Q) cudaStreamSynchronize(sU);
   const double t2 = sn::now_ms();
   if (rc == SN_OK || rc == SN_ERR_REJECTED) {
-    if (cudaMemcpy2DAsync(S, ldS * 8, dS, n * 8, n * 8, n, cudaMemcpyDeviceToHost, sA) != cudaSuccess ||
-        (Q && cudaMemcpy2DAsync(Q, ldQ * 8, dQ, n * 8, n * 8, n, cudaMemcpyDeviceToHost, sA) != cudaSuccess) ||
+    if (copy(S, ldS, dS, n, cudaMemcpyDeviceToHost, sA) != cudaSuccess ||
+        (Q && copy(Q, ldQ, dQ, n, cudaMemcpyDeviceToHost, sA) != cudaSuccess) ||
         cudaStreamSynchronize(sA) != cudaSuccess)
       rc = SN_ERR_CUDA;
   }
@@ -606,7 +623,7 @@ int sn_reorder_schur_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS, 
   cudaFree(dS);
   if (dQ) cudaFree(dQ);
   if (stats) {
-    stats->ms_h2d = t1 - t0;
+    stats->ms_h2d = t1 - t0;     // issue time of the uploads (they overlap the run)
     stats->ms_d2h = t3 - t2;
     stats->ms_total = t3 - t0;
   }
