@@ -148,7 +148,9 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
   using C = TCfg<MT>;
   constexpr bool LEFT = (KIND == 0);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // align by an offset into the shared array itself (keeps the pointer in the shared window,
+  // so fragment loads compile to LDS rather than generic loads)
+  unsigned char* smem = smem_raw + ((1024u - (sa(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = (uint64_t*)(smem + (size_t)C::STAGE * C::NS);
   uint64_t* empty = full + C::NS;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
