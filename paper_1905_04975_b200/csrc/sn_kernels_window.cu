@@ -18,7 +18,7 @@
 namespace sn {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;   // 4 transform warps + 8 apply warps (the DMMA tiles use warps 0-7)
 constexpr int LDD = 65;   // inner window (odd stride: conflict-free row walks)
 constexpr int LDZ = 68;   // inner accumulator (== 4 mod 16: conflict-free DMMA fragments)
 constexpr int LDT = 68;   // staging tile
@@ -105,6 +105,7 @@ __device__ void inner_update(double* P, int64_t ld, int64_t r0, int64_t c0, int 
       }
     }
     __syncthreads();
+    if (warp >= 8) continue;   // 4 (M) x 2 (N) warps per 64 x 64 tile
     double acc[4][4];
     tile_mma<LEFT>(Tb, Zin, kpad, acc, warp, lane);
 #pragma unroll
@@ -128,30 +129,44 @@ __device__ void inner_update(double* P, int64_t ld, int64_t r0, int64_t c0, int 
 // Mover i (i-th selected block of [top, bottom), top to bottom) starts at block P_i, passes
 // the u_i unselected blocks above it and ends at block top+i.  It performs its s-th swap at
 // step 2i + s, so concurrent swaps are at least two blocks apart: their index sets are
-// disjoint and their orthogonal factors commute.  Per step:
-//   A  transforms of all active swaps, one thread per swap, warp w <-> swap type w
-//   B  left applications (rows right of each block) + new diagonal blocks, a warp per swap
-//   C  right applications (columns above each block, accumulator columns), a warp per swap
-// with a CTA barrier after each phase.  Warp 0 prepares the next step's lists during C.
+// disjoint and their orthogonal factors commute.
+//
+// Software pipeline: while the apply warps perform step t -- (B) the row applications, then,
+// after a barrier among themselves, (C) the column applications to the window and to Zin --
+// the transform warps already evaluate the transforms of step t+1, one thread per swap
+// grouped by type (a lane pair per 2x2|2x2 swap).  This is legal because the transform of
+// mover i's step-(t+1) swap reads only (a) the diagonal block of the unselected block u it
+// passes next, last written two or more steps earlier by mover i-1, (b) mover i's new
+// diagonal block, which is part of its step-t record, and (c) the coupling rows of u in the
+// columns of mover i's step-t pair, which only mover i's step-t column application changes:
+// the transform thread applies that column transform to those rows itself (and writes them
+// back), and the apply warps skip them.  One CTA barrier per step.
+constexpr int kWT = 4;                     // transform warps: w < 3 swap type w, w = 3 2x2|2x2
+constexpr int kWA = kThreads / 32 - kWT;   // apply warps
+constexpr int kRecBuf = 4 * 32 * dev::kRec;   // doubles per record buffer (type x slot)
+
 struct WaveShared {
   int M, U, T;                        // movers, unselected blocks, steps
   uint8_t msz[64], usz[64];           // sizes of movers / unselected blocks (top to bottom)
   int16_t mpos[64], mu[64];           // initial block position, unselected blocks above
   int16_t mrows[65], urows[65];       // row prefixes of movers / unselected blocks
-  int16_t lj[2][4][32];               // per step parity, type, slot: local row j
-  int8_t lflat[2][4][32];             // ... flat index (mover order among active swaps)
-  int8_t ftype[2][64], fslot[2][64], fmover[2][64];
-  int cnt[2][4], nflat[2];
-  int8_t frej[64];
-  int anyrej, done, laststep;
+  // step lists, triple-buffered by t % 3 (step t applied, t+1 transformed, t+2 prepared)
+  int16_t lj[3][4][32];               // per type, slot: local row j
+  int8_t lflat[3][4][32];             // ... flat index (mover order among active swaps)
+  int8_t ftype[3][64], fslot[3][64], fmover[3][64];
+  int8_t mflat[3][32];                // mover -> flat index of its swap in the step, or -1
+  int cnt[3][4], nflat[3];
+  int8_t frej[3][64];
+  int anyrej[3];
+  int done, laststep, rejected;
   int8_t zlo[64], zhi[64];            // nonzero row interval of every column of Zin
-  unsigned long long bmax, bmax_sum, amax, amax_sum;  // debug timing (tprof)
   int rej_row, rej_n1, rej_n2;
+  unsigned long long tmax[2], tsum[2];  // debug timing (tprof): per-step max of each role
 };
 
 __device__ void wave_prepare(WaveShared& W, int t, int lane) {
-  // warp 0 only: lists of the active swaps of step t, grouped by type and in mover order
-  const int buf = t & 1;
+  // one warp: lists of the active swaps of step t, grouped by type and in mover order
+  const int buf = t % 3;
   const int i = lane;
   bool act = false;
   int ty = 0, j = 0;
@@ -167,6 +182,7 @@ __device__ void wave_prepare(WaveShared& W, int t, int lane) {
   const unsigned amask = __ballot_sync(0xffffffffu, act);
   const unsigned lt = (1u << lane) - 1u;
   const int flat = __popc(amask & lt);
+  W.mflat[buf][lane] = act ? (int8_t)flat : (int8_t)-1;
   for (int q = 0; q < 4; ++q) {
     const unsigned tm = __ballot_sync(0xffffffffu, act && ty == q);
     if (act && ty == q) {
@@ -182,14 +198,122 @@ __device__ void wave_prepare(WaveShared& W, int t, int lane) {
   if (lane == 0) W.nflat[buf] = __popc(amask);
 }
 
-// debug timing (WindowArgs::tprof): cycles of tid 0 per phase, summed over windows
-// [0] A transforms, [1] B rows, [2] C columns, [3] step tail, [4] steps, [5] wave setup,
-// [6] staging, [7] write-back + inner updates, [8] kernel total, [9] windows
-__device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Din, double* Zin,
+// The (n1+n2)^2 block of a step-t swap (type ty at local row j, flat index `flat`): from the
+// window directly for a mover's first swap, else assembled from the window (the unselected
+// block), the mover's step t-1 record (its new diagonal block) and the coupling rows, to which
+// the step t-1 column transform is applied here (returned in cpl for the write-back).
+__device__ __forceinline__ int wave_assemble(int t, int ty, int j, int flat, const double* Din, const double* recs,
+                                             const WaveShared& W, double (&Db)[4][4], double (&cpl)[2][4],
+                                             int& jp, int& pnd) {
+  const int n1 = (ty >> 1) + 1, n2 = (ty & 1) + 1, nd = n1 + n2;
+  const int i = W.fmover[t % 3][flat];
+  const int pf = t > 0 ? W.mflat[(t - 1) % 3][i] : -1;
+  if (pf < 0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) Db[r][c] = (r < nd && c < nd) ? Din[(j + r) + (j + c) * LDD] : 0.0;
+    return 0;
+  }
+  const int psb = (t - 1) % 3;
+  const int pt = W.ftype[psb][pf], ps = W.fslot[psb][pf];
+  const double* prec = recs + ((t - 1) & 1) * kRecBuf + (pt * 32 + ps) * dev::kRec;
+  jp = W.lj[psb][pt][ps];                      // == j + n1: mover i's previous pair
+  pnd = (pt >> 1) + (pt & 1) + 2;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) Db[r][c] = 0.0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    if (r >= n1) break;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      if (c < n1) Db[r][c] = Din[(j + r) + (j + c) * LDD];
+    double x[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < pnd) x[c] = Din[(j + r) + (jp + c) * LDD];
+    dev::rec_apply_row_t(pt, x, prec);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cpl[r][c] = x[c];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      if (c < n2) Db[r][n1 + c] = x[c];
+  }
+  if (pt == 0) {
+    Db[n1][n1] = prec[3];                      // a moved 1x1 keeps its exact value (R7)
+  } else {
+#pragma unroll
+    for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+      for (int b2 = 0; b2 < 2; ++b2)
+        if (a2 < n2 && b2 < n2) Db[n1 + a2][n1 + b2] = prec[10 + a2 + 4 * b2];
+  }
+  return n1;
+}
+
+__device__ __forceinline__ void wave_writeback(int nrows, int jp, int pnd, int j, double* Din,
+                                               const double (&cpl)[2][4]) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+    if (r < nrows) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < pnd) Din[(j + r) + (jp + c) * LDD] = cpl[r][c];
+    }
+}
+
+// transforms of step t by the transform warps
+__device__ void wave_transform(int t, int base, double* Din, double* recs, WaveShared& W, int warp, int lane,
+                               bool force_here, int force_swap) {
+  const int sb = t % 3;
+  double* rec_t = recs + (t & 1) * kRecBuf;
+  if (warp < 3) {
+    if (lane < W.cnt[sb][warp]) {
+      const int ty = warp;
+      const int j = W.lj[sb][ty][lane];
+      const int flat = W.lflat[sb][ty][lane];
+      double Db[4][4], cpl[2][4];
+      int jp = 0, pnd = 0;
+      const int nw = wave_assemble(t, ty, j, flat, Din, recs, W, Db, cpl, jp, pnd);
+      wave_writeback(nw, jp, pnd, j, Din, cpl);
+      bool rj = force_here && (base + flat == force_swap);
+      if (!rj) rj = dev::swap_compute_blk_t(ty, Db, rec_t + (ty * 32 + lane) * dev::kRec);
+      W.frej[sb][flat] = rj ? 1 : 0;
+      if (rj) atomicOr(&W.anyrej[sb], 1);
+    }
+  } else if (warp == 3) {
+    const int c3 = W.cnt[sb][3];
+    for (int b0 = 0; b0 < c3; b0 += 16) {
+      const int slot = b0 + (lane >> 1), role = lane & 1;
+      const bool act = slot < c3;
+      const int sl = act ? slot : b0;
+      const int j = W.lj[sb][3][sl];
+      const int flat = W.lflat[sb][3][sl];
+      double Db[4][4], cpl[2][4];
+      int jp = 0, pnd = 0;
+      const int nw = wave_assemble(t, 3, j, flat, Din, recs, W, Db, cpl, jp, pnd);
+      __syncwarp();   // every lane has read the coupling rows before they are written back
+      if (act && role == 0) wave_writeback(nw, jp, pnd, j, Din, cpl);
+      double tmp[dev::kRec];
+      bool rj = dev::swap_compute_22_paired_blk(Db, tmp, role);
+      if (act && role == 0) {
+        rj = rj || (force_here && (base + flat == force_swap));
+        double* dst = rec_t + (3 * 32 + slot) * dev::kRec;
+#pragma unroll
+        for (int q = 0; q < dev::kRec; ++q) dst[q] = tmp[q];
+        W.frej[sb][flat] = rj ? 1 : 0;
+        if (rj) atomicOr(&W.anyrej[sb], 1);
+      }
+    }
+  }
+}
+
+__device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Din, double* Zin, double* recs,
                                 WaveShared& W, int tid, int warp, int lane, bool force_here, int force_swap,
                                 int done_before, unsigned long long* tp) {
-  long long c0 = tp && tid == 0 ? clock64() : 0, cA = 0, cB = 0, cC = 0, cT = 0, cS = 0, cBw = 0;
-  __shared__ double rec[4][32][dev::kRec];
+  const long long c0 = tp && tid == 0 ? clock64() : 0;
   if (tid == 0) {
     // movers / unselected lists of the inner window (block list in s_bsz/s_bsel)
     int M = 0, U = 0, T = 0;
@@ -209,143 +333,112 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
       }
     }
     W.M = M; W.U = U; W.T = T;
-    W.anyrej = 0; W.laststep = -1;
-    W.done = done_before;
+    W.anyrej[0] = W.anyrej[1] = W.anyrej[2] = 0;
+    W.rejected = 0;
+    W.tmax[0] = W.tmax[1] = W.tsum[0] = W.tsum[1] = 0;
   }
   if (tid < kInner) { W.zlo[tid] = (int8_t)tid; W.zhi[tid] = (int8_t)tid; }
-  if (tid == 0) { W.bmax = 0; W.bmax_sum = 0; W.amax = 0; W.amax_sum = 0; }
   __syncthreads();
-  if (warp == 0) wave_prepare(W, 0, lane);
-  __syncthreads();
-  if (tp && tid == 0) { const long long c = clock64(); cS = c - c0; c0 = c; }
   const int T = W.T;
+  if (warp == 0) wave_prepare(W, 0, lane);
+  if (warp == 1 && T > 1) wave_prepare(W, 1, lane);
+  __syncthreads();
+  int base = done_before;
+  if (warp < kWT) wave_transform(0, base, Din, recs, W, warp, lane, force_here, force_swap);
+  __syncthreads();
   int t = 0;
+  bool stop_now = false;
   for (; t < T; ++t) {
-    const int buf = t & 1;
-    const int base = W.done;
-    // A: transforms, one thread per swap (a lane pair per 2x2|2x2 swap)
-    if (warp < 3 && lane < W.cnt[buf][warp]) {
-      const int j = W.lj[buf][warp][lane];
-      const int flat = W.lflat[buf][warp][lane];
-      bool rj = force_here && (base + flat == force_swap);
-      const long long ta = tp ? clock64() : 0;
-      if (!rj) rj = dev::swap_compute_t(warp, Din, LDD, j, rec[warp][lane]);
-      if (tp) atomicMax(&W.amax, (unsigned long long)(clock64() - ta));
-      W.frej[flat] = rj ? 1 : 0;
-      if (rj) atomicOr(&W.anyrej, 1);
-    } else if (warp == kThreads / 32 - 1) {
-      // the last warp (idle in phase A) prepares the next step's swap lists (double-buffered
-      // by step parity; they depend only on the inner window's static mover/unselected lists)
-      if (t + 1 < T) wave_prepare(W, t + 1, lane);
-    } else if (warp == 3) {
-      const int c3 = W.cnt[buf][3];
-      for (int b0 = 0; b0 < c3; b0 += 16) {
-        const int slot = b0 + (lane >> 1), role = lane & 1;
-        const bool act = slot < c3;
-        const int sl = act ? slot : b0;
-        const int j = W.lj[buf][3][sl];
-        double tmp[dev::kRec];
-        const long long ta = tp ? clock64() : 0;
-        bool rj = dev::swap_compute_22_paired(Din, LDD, j, tmp, role);
-        if (tp) atomicMax(&W.amax, (unsigned long long)(clock64() - ta));
-        if (act && role == 0) {
-          const int flat = W.lflat[buf][3][slot];
-          rj = rj || (force_here && (base + flat == force_swap));
-#pragma unroll
-          for (int q = 0; q < dev::kRec; ++q) rec[3][slot][q] = tmp[q];
-          W.frej[flat] = rj ? 1 : 0;
-          if (rj) atomicOr(&W.anyrej, 1);
+    const int sb = t % 3;
+    stop_now = W.anyrej[sb] != 0;          // a swap of step t was rejected: apply the rest, stop
+    const bool last = stop_now || t + 1 == T;
+    const int nf = W.nflat[sb];
+    if (tid == 0) W.anyrej[(t + 2) % 3] = 0;
+    const long long cs = tp ? clock64() : 0;
+    if (warp < kWT) {
+      if (!last) wave_transform(t + 1, base + nf, Din, recs, W, warp, lane, force_here, force_swap);
+    } else {
+      const double* rec_t = recs + (t & 1) * kRecBuf;
+      const int aw = warp - kWT;
+      // B: rows
+      for (int f = aw; f < nf; f += kWA) {
+        if (W.frej[sb][f]) continue;
+        const int ty = W.ftype[sb][f], sl = W.fslot[sb][f];
+        dev::swap_apply_rows_t(ty, Din, LDD, kin, W.lj[sb][ty][sl], rec_t + (ty * 32 + sl) * dev::kRec, lane);
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(kWA * 32) : "memory");
+      // C: columns of the window (less the coupling rows the next transform applies) and of Zin
+      for (int f = aw; f < nf; f += kWA) {
+        if (W.frej[sb][f]) continue;
+        const int ty = W.ftype[sb][f], sl = W.fslot[sb][f];
+        const int j = W.lj[sb][ty][sl];
+        const double* rec = rec_t + (ty * 32 + sl) * dev::kRec;
+        int rows = j;
+        if (!last) {
+          const int nf1 = W.mflat[(t + 1) % 3][W.fmover[sb][f]];
+          if (nf1 >= 0) rows = j - ((W.ftype[(t + 1) % 3][nf1] >> 1) + 1);
+        }
+        dev::swap_apply_cols_t(ty, Din, LDD, rows, j, rec, lane);
+        {
+          // Zin columns j..j+nd-1 are zero outside the union of their row intervals (Zin starts
+          // as I and every swap mixes adjacent columns): apply the transform there only
+          const int nd = (ty >> 1) + (ty & 1) + 2;
+          int lo = W.zlo[j], hi = W.zhi[j];
+          for (int c = 1; c < nd; ++c) { lo = min(lo, (int)W.zlo[j + c]); hi = max(hi, (int)W.zhi[j + c]); }
+          dev::swap_apply_cols_t(ty, Zin + lo, LDZ, hi - lo + 1, j, rec, lane);
+          __syncwarp();
+          if (lane < nd) { W.zlo[j + lane] = (int8_t)lo; W.zhi[j + lane] = (int8_t)hi; }
+        }
+        {
+          // the swap mixes outer Z columns i1+j .. i1+j+n1+n2-1 (concurrent swaps: disjoint);
+          // lanes 0..3 hold one column each, reduced over groups of 4 lanes
+          const int c = i1 + j + (lane & 3), nc = (ty >> 1) + (ty & 1) + 2;
+          const bool mine = (lane & 3) < nc;
+          int lo = mine ? g_zlo[c] : kZld, hi = mine ? g_zhi[c] : -1;
+          lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+          hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+          lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
+          hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
+          if (lane < 4 && mine) { g_zlo[c] = (int16_t)lo; g_zhi[c] = (int16_t)hi; }
         }
       }
+      // the last apply warp prepares the lists of step t+2 (buffer (t+2) % 3 is idle)
+      if (warp == kThreads / 32 - 1 && t + 2 < T) wave_prepare(W, t + 2, lane);
     }
-    __syncthreads();
-    if (tp && tid == 0) { const long long c = clock64(); cA += c - c0; c0 = c; }
-    const int nf = W.nflat[buf];
-    // B: rows
-    const long long cb0 = tp && lane == 0 ? clock64() : 0;
-    for (int f = warp; f < ((g_wdbg & 1) ? 0 : nf); f += kThreads / 32) {
-      if (W.frej[f]) continue;
-      const int ty = W.ftype[buf][f], sl = W.fslot[buf][f];
-      dev::swap_apply_rows_t(ty, Din, LDD, kin, W.lj[buf][ty][sl], rec[ty][sl], lane);
-    }
-    if (tp && lane == 0) {
-      const long long d = clock64() - cb0;
-      cBw += d;
-      atomicMax(&W.bmax, (unsigned long long)d);
-    }
-    __syncthreads();
-    if (tp && tid == 0) { const long long c = clock64(); cB += c - c0; c0 = c; }
-    // C: columns of the window and of the accumulator
-    for (int f = warp; f < ((g_wdbg & 2) ? 0 : nf); f += kThreads / 32) {
-      if (W.frej[f]) continue;
-      const int ty = W.ftype[buf][f], sl = W.fslot[buf][f];
-      const int j = W.lj[buf][ty][sl];
-      dev::swap_apply_cols_t(ty, Din, LDD, j, j, rec[ty][sl], lane);
-      {
-        // Zin columns j..j+nd-1 are zero outside the union of their row intervals (Zin starts
-        // as I and every swap mixes adjacent columns): apply the transform there only
-        const int nd = (ty >> 1) + (ty & 1) + 2;
-        int lo = W.zlo[j], hi = W.zhi[j];
-        for (int c = 1; c < nd; ++c) { lo = min(lo, (int)W.zlo[j + c]); hi = max(hi, (int)W.zhi[j + c]); }
-        dev::swap_apply_cols_t(ty, Zin + lo, LDZ, hi - lo + 1, j, rec[ty][sl], lane);
-        __syncwarp();
-        if (lane < nd) { W.zlo[j + lane] = (int8_t)lo; W.zhi[j + lane] = (int8_t)hi; }
-      }
-      {
-        // the swap mixes outer Z columns i1+j .. i1+j+n1+n2-1 (concurrent swaps: disjoint);
-        // lanes 0..3 hold one column each, reduced over groups of 4 lanes
-        const int c = i1 + j + (lane & 3), nc = (ty >> 1) + (ty & 1) + 2;
-        const bool mine = (lane & 3) < nc;
-        int lo = mine ? g_zlo[c] : kZld, hi = mine ? g_zhi[c] : -1;
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
-        if (lane < 4 && mine) { g_zlo[c] = (int16_t)lo; g_zhi[c] = (int16_t)hi; }
-      }
-    }
-    const bool stop = W.anyrej != 0;
-    if (tid == 0 && !stop) {
-      // common case (nothing rejected): the step's bookkeeping, no extra barrier
-      W.done = base + nf;
-      W.laststep = t;
-    }
+    if (tp && lane == 0) atomicMax(&W.tmax[warp < kWT ? 0 : 1], (unsigned long long)(clock64() - cs));
     __syncthreads();
     if (tp && tid == 0) {
-      const long long c = clock64(); cC += c - c0; c0 = c;
-      W.bmax_sum += W.bmax;
-      W.bmax = 0;
-      W.amax_sum += W.amax;
-      W.amax = 0;
+      W.tsum[0] += W.tmax[0]; W.tsum[1] += W.tmax[1];
+      W.tmax[0] = 0; W.tmax[1] = 0;
     }
-    if (stop) {
-      if (tid == 0) {
-        int nrej = 0, first = -1;
-        for (int f = 0; f < nf; ++f)
-          if (W.frej[f]) { ++nrej; if (first < 0) first = f; }
-        W.done += nf - nrej;
-        if (first >= 0) {
-          const int ty = W.ftype[buf][first], sl = W.fslot[buf][first];
-          W.rej_row = i1 + W.lj[buf][ty][sl];   // window-local row
-          W.rej_n1 = (ty >> 1) + 1;
-          W.rej_n2 = (ty & 1) + 1;
-        }
-        W.laststep = t;
-      }
-      __syncthreads();
-      break;
+    if (stop_now) break;
+    base += nf;
+  }
+  if (tid == 0) {
+    const int tl = min(t, T - 1);
+    W.laststep = tl;
+    if (stop_now) {
+      const int sb = tl % 3;
+      int nrej = 0, first = -1;
+      for (int f = 0; f < W.nflat[sb]; ++f)
+        if (W.frej[sb][f]) { ++nrej; if (first < 0) first = f; }
+      W.done = base + W.nflat[sb] - nrej;
+      const int ty = W.ftype[sb][first], sl = W.fslot[sb][first];
+      W.rej_row = i1 + W.lj[sb][ty][sl];   // window-local row
+      W.rej_n1 = (ty >> 1) + 1;
+      W.rej_n2 = (ty & 1) + 1;
+      W.rejected = 1;
+    } else {
+      W.done = base;
+    }
+    if (tp) {
+      atomicAdd(&tp[1], (unsigned long long)(clock64() - c0));
+      atomicAdd(&tp[4], (unsigned long long)T);
+      atomicAdd(&tp[0], W.tsum[0]);   // transform side, per-step max summed
+      atomicAdd(&tp[2], W.tsum[1]);   // apply side
     }
   }
-  if (tp && tid == 0) {
-    atomicAdd(&tp[0], (unsigned long long)cA); atomicAdd(&tp[1], (unsigned long long)cB);
-    atomicAdd(&tp[2], (unsigned long long)cC); atomicAdd(&tp[3], (unsigned long long)cT);
-    atomicAdd(&tp[4], (unsigned long long)t); atomicAdd(&tp[5], (unsigned long long)cS);
-  }
-  if (tp && lane == 0) {
-    atomicAdd(&tp[10], (unsigned long long)cBw);   // summed over the 8 warps
-    if (tid == 0) atomicAdd(&tp[11], W.bmax_sum);   // per step max over warps, summed
-    if (tid == 0) atomicAdd(&tp[12], W.amax_sum);   // per step max transform latency, summed
-  }
+  __syncthreads();
   // new block arrangement of [top, bottom)
   if (tid == 0) {
     uint8_t nsz[64], nsel[64];
@@ -355,14 +448,14 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
     const int tl = W.laststep;
     for (int i = 0; i < W.M; ++i) {
       int applied = W.mu[i];
-      if (W.anyrej) {
+      if (W.rejected) {
         applied = min(max(tl + 1 - 2 * i, 0), (int)W.mu[i]);
         // a rejected swap of this mover at the last step was not applied
         const int s = tl - 2 * i;
         if (s >= 0 && s < W.mu[i]) {
-          const int buf = tl & 1;
+          const int buf = tl % 3;
           for (int f = 0; f < W.nflat[buf]; ++f)
-            if (W.fmover[buf][f] == i && W.frej[f]) { applied -= 1; break; }
+            if (W.fmover[buf][f] == i && W.frej[buf][f]) { applied -= 1; break; }
         }
       }
       const int pos = W.mpos[i] - top - applied;
@@ -382,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
   double* Din = smem;                       // kInner x LDD
   double* Zin = Din + kInner * LDD;         // kInner x LDZ
   double* Tb = Zin + kInner * LDZ;          // 64 x LDT
+  double* recs = Tb + 64 * LDT;             // transform records, 2 step buffers x 4 types x 32
   __shared__ WaveShared W;
   uint8_t* bsz = g_bsz;
   uint8_t* bsel = g_bsel;
@@ -416,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
   }
   __syncthreads();
   if (tid == 0) {
-    W.anyrej = 0;
+    W.rejected = 0;
     int r = 0;
     for (int b = 0; b < nb; ++b) { brow[b] = (int16_t)r; r += bsz[b]; }
     brow[nb] = (int16_t)r;
@@ -438,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
     }
     __syncthreads();
     if (a.tprof && tid == 0) { const long long c = clock64(); atomicAdd(&a.tprof[6], (unsigned long long)(c - ck)); ck = c; }
-    wavefront_swaps(top, bottom, i1, kin, Din, Zin, W, tid, warp, lane, wd.order == a.force_order,
+    wavefront_swaps(top, bottom, i1, kin, Din, Zin, recs, W, tid, warp, lane, wd.order == a.force_order,
                     a.force_swap, swaps_done, a.tprof);
     if (a.tprof && tid == 0) ck = clock64();
     swaps_done = W.done;
@@ -453,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
     inner_update<false>(Z, kZld, 0, i1, k, kin, Zin, Tb, tid);                   // Z columns
     __syncthreads();
     if (a.tprof && tid == 0) { const long long c = clock64(); atomicAdd(&a.tprof[7], (unsigned long long)(c - ck)); ck = c; }
-    if (W.anyrej) break;
+    if (W.rejected) break;
   }
   {
     int16_t* zr = a.zrange + (int64_t)wd.slot * kZrange;
@@ -483,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
     atomicAdd(&a.tprof[9], 1ull);
   }
   if (tid == 0) {
-    if (W.anyrej) {
+    if (W.rejected) {
       a.ctl->abort = 1;
       a.ctl->rej_window = sidx;
       a.ctl->rej_swaps_done = swaps_done;
@@ -501,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
 }  // namespace
 
 size_t window_smem_bytes() {
-  return sizeof(double) * (size_t)(kInner * LDD + kInner * LDZ + 64 * LDT);
+  return sizeof(double) * (size_t)(kInner * LDD + kInner * LDZ + 64 * LDT + 2 * kRecBuf);
 }
 
 void launch_window(const WindowArgs& a, cudaStream_t st) {
