@@ -455,10 +455,10 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
     cudaFree(dtp);
     const double nwin = (double)(h[9] ? h[9] : 1);
     std::fprintf(stderr,
-                 "{\"probe\":\"window_phases\",\"windows\":%llu,\"steps_per_window\":%.1f,\"cycles_per_window\":"
+                 "{\"probe\":\"window_phases\",\"assembly_max\":%.0f,\"transform_max\":%.0f,\"windows\":%llu,\"steps_per_window\":%.1f,\"cycles_per_window\":"
                  "{\"A\":%.0f,\"B\":%.0f,\"C\":%.0f,\"wave_setup\":%.0f,\"staging\":%.0f,\"inner_updates\":%.0f,"
                  "\"total\":%.0f,\"B_work_avg_warp\":%.0f,\"B_work_max_warp\":%.0f,\"A_transform_max\":%.0f}}\n",
-                 h[9], h[4] / nwin, h[0] / nwin, h[1] / nwin, h[2] / nwin, h[5] / nwin, h[6] / nwin, h[7] / nwin,
+                 h[13] / nwin, h[14] / nwin, h[9], h[4] / nwin, h[0] / nwin, h[1] / nwin, h[2] / nwin, h[5] / nwin, h[6] / nwin, h[7] / nwin,
                  h[8] / nwin, h[10] / nwin / 8.0, h[11] / nwin, h[12] / nwin);
   }
 

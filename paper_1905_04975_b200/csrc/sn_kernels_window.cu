@@ -18,12 +18,13 @@
 namespace sn {
 namespace {
 
-constexpr int kThreads = 384;   // 4 transform warps + 8 apply warps (the DMMA tiles use warps 0-7)
+constexpr int kThreads = 256;   // 4 transform warps + 4 apply warps (the DMMA tiles use warps 0-7)
 constexpr int LDD = 65;   // inner window (odd stride: conflict-free row walks)
 constexpr int LDZ = 68;   // inner accumulator (== 4 mod 16: conflict-free DMMA fragments)
 constexpr int LDT = 68;   // staging tile
 
-__device__ int g_wdbg;   // debug: 1 skip phase B, 2 skip phase C (timing experiments only)
+__device__ int g_wdbg;
+__device__ int g_tprof_on;   // debug timing switch (set with WindowArgs::tprof)   // debug: 1 skip phase B, 2 skip phase C (timing experiments only)
 
 // block list of the window being processed (one CTA per window)
 __shared__ uint8_t g_bsz[256], g_bsel[256];
@@ -155,13 +156,15 @@ struct WaveShared {
   int8_t lflat[3][4][32];             // ... flat index (mover order among active swaps)
   int8_t ftype[3][64], fslot[3][64], fmover[3][64];
   int8_t mflat[3][32];                // mover -> flat index of its swap in the step, or -1
+  int16_t lprev[3][4][32];            // per type, slot: the mover's previous record (type*32 +
+                                      // slot, in the other record buffer), or -1 (first swap)
   int cnt[3][4], nflat[3];
   int8_t frej[3][64];
   int anyrej[3];
   int done, laststep, rejected;
   int8_t zlo[64], zhi[64];            // nonzero row interval of every column of Zin
   int rej_row, rej_n1, rej_n2;
-  unsigned long long tmax[2], tsum[2];  // debug timing (tprof): per-step max of each role
+  unsigned long long tmax[4], tsum[4];  // debug timing (tprof): per-step maxima
 };
 
 __device__ void wave_prepare(WaveShared& W, int t, int lane) {
@@ -187,6 +190,12 @@ __device__ void wave_prepare(WaveShared& W, int t, int lane) {
     const unsigned tm = __ballot_sync(0xffffffffu, act && ty == q);
     if (act && ty == q) {
       const int slot = __popc(tm & lt);
+      int pv = -1;
+      if (t > 0) {
+        const int pb = (t - 1) % 3, pf = W.mflat[pb][i];   // lists of t-1 are already prepared
+        if (pf >= 0) pv = W.ftype[pb][pf] * 32 + W.fslot[pb][pf];
+      }
+      W.lprev[buf][q][slot] = (int16_t)pv;
       W.lj[buf][q][slot] = (int16_t)j;
       W.lflat[buf][q][slot] = (int8_t)flat;
       W.ftype[buf][flat] = (int8_t)q;
@@ -202,66 +211,81 @@ __device__ void wave_prepare(WaveShared& W, int t, int lane) {
 // window directly for a mover's first swap, else assembled from the window (the unselected
 // block), the mover's step t-1 record (its new diagonal block) and the coupling rows, to which
 // the step t-1 column transform is applied here (returned in cpl for the write-back).
-__device__ __forceinline__ int wave_assemble(int t, int ty, int j, int flat, const double* Din, const double* recs,
-                                             const WaveShared& W, double (&Db)[4][4], double (&cpl)[2][4],
-                                             int& jp, int& pnd) {
-  const int n1 = (ty >> 1) + 1, n2 = (ty & 1) + 1, nd = n1 + n2;
-  const int i = W.fmover[t % 3][flat];
-  const int pf = t > 0 ? W.mflat[(t - 1) % 3][i] : -1;
-  if (pf < 0) {
+template <int N1, int N2>
+__device__ __forceinline__ int wave_assemble(int t, int j, int pv, const double* Din, const double* recs,
+                                             double (&Db)[4][4], double (&cpl)[2][4], int& jp, int& pnd) {
+  constexpr int nd = N1 + N2;
+  if (pv < 0) {
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) Db[r][c] = (r < nd && c < nd) ? Din[(j + r) + (j + c) * LDD] : 0.0;
     return 0;
   }
-  const int psb = (t - 1) % 3;
-  const int pt = W.ftype[psb][pf], ps = W.fslot[psb][pf];
-  const double* prec = recs + ((t - 1) & 1) * kRecBuf + (pt * 32 + ps) * dev::kRec;
-  jp = W.lj[psb][pt][ps];                      // == j + n1: mover i's previous pair
+  const int pt = pv >> 5;
+  const double* prec = recs + ((t - 1) & 1) * kRecBuf + pv * dev::kRec;
+  jp = j + N1;                                 // mover i's previous pair
   pnd = (pt >> 1) + (pt & 1) + 2;
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) Db[r][c] = 0.0;
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    if (r >= n1) break;
+  for (int r = 0; r < N1; ++r) {
 #pragma unroll
-    for (int c = 0; c < 2; ++c)
-      if (c < n1) Db[r][c] = Din[(j + r) + (j + c) * LDD];
-    double x[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int c = 0; c < N1; ++c) Db[r][c] = Din[(j + r) + (j + c) * LDD];
+    double x[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-      if (c < pnd) x[c] = Din[(j + r) + (jp + c) * LDD];
+    for (int c = 0; c < 4; ++c) x[c] = c < pnd ? Din[(j + r) + (jp + c) * LDD] : 0.0;
     dev::rec_apply_row_t(pt, x, prec);
 #pragma unroll
     for (int c = 0; c < 4; ++c) cpl[r][c] = x[c];
 #pragma unroll
-    for (int c = 0; c < 2; ++c)
-      if (c < n2) Db[r][n1 + c] = x[c];
+    for (int c = 0; c < N2; ++c) Db[r][N1 + c] = x[c];
   }
   if (pt == 0) {
-    Db[n1][n1] = prec[3];                      // a moved 1x1 keeps its exact value (R7)
+    Db[N1][N1] = prec[3];                      // a moved 1x1 keeps its exact value (R7)
   } else {
 #pragma unroll
-    for (int a2 = 0; a2 < 2; ++a2)
+    for (int a2 = 0; a2 < N2; ++a2)
 #pragma unroll
-      for (int b2 = 0; b2 < 2; ++b2)
-        if (a2 < n2 && b2 < n2) Db[n1 + a2][n1 + b2] = prec[10 + a2 + 4 * b2];
+      for (int b2 = 0; b2 < N2; ++b2) Db[N1 + a2][N1 + b2] = prec[10 + a2 + 4 * b2];
   }
-  return n1;
+  return N1;
 }
 
-__device__ __forceinline__ void wave_writeback(int nrows, int jp, int pnd, int j, double* Din,
-                                               const double (&cpl)[2][4]) {
+template <int N1>
+__device__ __forceinline__ void wave_writeback(int jp, int pnd, int j, double* Din, const double (&cpl)[2][4]) {
 #pragma unroll
-  for (int r = 0; r < 2; ++r)
-    if (r < nrows) {
+  for (int r = 0; r < N1; ++r)
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (c < pnd) Din[(j + r) + (jp + c) * LDD] = cpl[r][c];
-    }
+    for (int c = 0; c < 4; ++c)
+      if (c < pnd) Din[(j + r) + (jp + c) * LDD] = cpl[r][c];
+}
+
+// one swap of type (N1, N2) by one thread (warps 0-2)
+template <int N1, int N2>
+__device__ __forceinline__ void wave_transform_one(int t, int base, int lane, double* Din, double* recs,
+                                                   WaveShared& W, bool force_here, int force_swap) {
+  constexpr int ty = (N1 - 1) * 2 + (N2 - 1);
+  const int sb = t % 3;
+  double* rec_t = recs + (t & 1) * kRecBuf;
+  const int j = W.lj[sb][ty][lane];
+  const int flat = W.lflat[sb][ty][lane];
+  double Db[4][4], cpl[2][4];
+  int jp = 0, pnd = 0;
+  const long long q0 = g_tprof_on ? clock64() : 0;
+  if (wave_assemble<N1, N2>(t, j, W.lprev[sb][ty][lane], Din, recs, Db, cpl, jp, pnd))
+    wave_writeback<N1>(jp, pnd, j, Din, cpl);
+  const long long q1 = g_tprof_on ? clock64() : 0;
+  bool rj = force_here && (base + flat == force_swap);
+  if (!rj) rj = dev::swap_compute_blk<N1, N2>(Db, rec_t + (ty * 32 + lane) * dev::kRec);
+  if (g_tprof_on) {
+    atomicMax(&W.tmax[2], (unsigned long long)(q1 - q0));
+    atomicMax(&W.tmax[3], (unsigned long long)(clock64() - q1));
+  }
+  W.frej[sb][flat] = rj ? 1 : 0;
+  if (rj) atomicOr(&W.anyrej[sb], 1);
 }
 
 // transforms of step t by the transform warps
@@ -271,17 +295,9 @@ __device__ void wave_transform(int t, int base, double* Din, double* recs, WaveS
   double* rec_t = recs + (t & 1) * kRecBuf;
   if (warp < 3) {
     if (lane < W.cnt[sb][warp]) {
-      const int ty = warp;
-      const int j = W.lj[sb][ty][lane];
-      const int flat = W.lflat[sb][ty][lane];
-      double Db[4][4], cpl[2][4];
-      int jp = 0, pnd = 0;
-      const int nw = wave_assemble(t, ty, j, flat, Din, recs, W, Db, cpl, jp, pnd);
-      wave_writeback(nw, jp, pnd, j, Din, cpl);
-      bool rj = force_here && (base + flat == force_swap);
-      if (!rj) rj = dev::swap_compute_blk_t(ty, Db, rec_t + (ty * 32 + lane) * dev::kRec);
-      W.frej[sb][flat] = rj ? 1 : 0;
-      if (rj) atomicOr(&W.anyrej[sb], 1);
+      if (warp == 0) wave_transform_one<1, 1>(t, base, lane, Din, recs, W, force_here, force_swap);
+      else if (warp == 1) wave_transform_one<1, 2>(t, base, lane, Din, recs, W, force_here, force_swap);
+      else wave_transform_one<2, 1>(t, base, lane, Din, recs, W, force_here, force_swap);
     }
   } else if (warp == 3) {
     const int c3 = W.cnt[sb][3];
@@ -293,11 +309,13 @@ __device__ void wave_transform(int t, int base, double* Din, double* recs, WaveS
       const int flat = W.lflat[sb][3][sl];
       double Db[4][4], cpl[2][4];
       int jp = 0, pnd = 0;
-      const int nw = wave_assemble(t, 3, j, flat, Din, recs, W, Db, cpl, jp, pnd);
+      const int nw = wave_assemble<2, 2>(t, j, W.lprev[sb][3][sl], Din, recs, Db, cpl, jp, pnd);
       __syncwarp();   // every lane has read the coupling rows before they are written back
-      if (act && role == 0) wave_writeback(nw, jp, pnd, j, Din, cpl);
+      if (act && role == 0 && nw) wave_writeback<2>(jp, pnd, j, Din, cpl);
       double tmp[dev::kRec];
+      const long long q1 = g_tprof_on ? clock64() : 0;
       bool rj = dev::swap_compute_22_paired_blk(Db, tmp, role);
+      if (g_tprof_on) atomicMax(&W.tmax[3], (unsigned long long)(clock64() - q1));
       if (act && role == 0) {
         rj = rj || (force_here && (base + flat == force_swap));
         double* dst = rec_t + (3 * 32 + slot) * dev::kRec;
@@ -335,13 +353,16 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
     W.M = M; W.U = U; W.T = T;
     W.anyrej[0] = W.anyrej[1] = W.anyrej[2] = 0;
     W.rejected = 0;
-    W.tmax[0] = W.tmax[1] = W.tsum[0] = W.tsum[1] = 0;
+    for (int q = 0; q < 4; ++q) { W.tmax[q] = 0; W.tsum[q] = 0; }
   }
   if (tid < kInner) { W.zlo[tid] = (int8_t)tid; W.zhi[tid] = (int8_t)tid; }
   __syncthreads();
   const int T = W.T;
-  if (warp == 0) wave_prepare(W, 0, lane);
-  if (warp == 1 && T > 1) wave_prepare(W, 1, lane);
+  if (warp == 0) {
+    wave_prepare(W, 0, lane);
+    __syncwarp();
+    if (T > 1) wave_prepare(W, 1, lane);   // reads step 0's lists
+  }
   __syncthreads();
   int base = done_before;
   if (warp < kWT) wave_transform(0, base, Din, recs, W, warp, lane, force_here, force_swap);
@@ -408,8 +429,7 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
     if (tp && lane == 0) atomicMax(&W.tmax[warp < kWT ? 0 : 1], (unsigned long long)(clock64() - cs));
     __syncthreads();
     if (tp && tid == 0) {
-      W.tsum[0] += W.tmax[0]; W.tsum[1] += W.tmax[1];
-      W.tmax[0] = 0; W.tmax[1] = 0;
+      for (int q = 0; q < 4; ++q) { W.tsum[q] += W.tmax[q]; W.tmax[q] = 0; }
     }
     if (stop_now) break;
     base += nf;
@@ -436,6 +456,8 @@ __device__ void wavefront_swaps(int top, int bottom, int i1, int kin, double* Di
       atomicAdd(&tp[4], (unsigned long long)T);
       atomicAdd(&tp[0], W.tsum[0]);   // transform side, per-step max summed
       atomicAdd(&tp[2], W.tsum[1]);   // apply side
+      atomicAdd(&tp[13], W.tsum[2]);   // assembly (max per step)
+      atomicAdd(&tp[14], W.tsum[3]);   // transform proper (max per step)
     }
   }
   __syncthreads();
@@ -607,6 +629,9 @@ void launch_window(const WindowArgs& a, cudaStream_t st) {
     return v;
   }();
   (void)wdbg;
+  static int tprof_state = -1;
+  const int want = a.tprof ? 1 : 0;
+  if (tprof_state != want) { cudaMemcpyToSymbol(g_tprof_on, &want, sizeof(int)); tprof_state = want; }
   const size_t smem = window_smem_bytes();
   if (!attr) {
     cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
