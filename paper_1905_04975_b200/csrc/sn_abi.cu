@@ -51,6 +51,8 @@ struct Workspace {
   DevBuf wins, pool, prefix, status, kwork, ctl, Z, zr, sub, bad;
   std::vector<cudaEvent_t> prof;   // event pool for opts.profile
   cudaStream_t sB = nullptr, sC = nullptr, sU = nullptr;   // sU: host->device upload of Q
+  cudaStream_t sH = nullptr;      // high priority: window tasks and the strips they wait for
+  cudaEvent_t evIn = nullptr, evOut = nullptr;
   cudaEvent_t evQup = nullptr;
   cudaEvent_t evW[kZgen] = {}, evQ[kZgen] = {}, evCrit[kZgen] = {}, evRest[kZgen] = {};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evJoin = nullptr, evJoinC = nullptr;
@@ -85,6 +87,9 @@ int ensure_runtime(Workspace& ws) {
     if (ws.sB) {
       cudaStreamDestroy(ws.sB);
       cudaStreamDestroy(ws.sC);
+      cudaStreamDestroy(ws.sH);
+      cudaStreamDestroy(ws.sU);
+      cudaEventDestroy(ws.evIn); cudaEventDestroy(ws.evOut); cudaEventDestroy(ws.evQup);
       for (int i = 0; i < kZgen; ++i) {
         cudaEventDestroy(ws.evW[i]); cudaEventDestroy(ws.evQ[i]);
         cudaEventDestroy(ws.evCrit[i]); cudaEventDestroy(ws.evRest[i]);
@@ -92,8 +97,16 @@ int ensure_runtime(Workspace& ws) {
       cudaEventDestroy(ws.ev0); cudaEventDestroy(ws.ev1);
       cudaEventDestroy(ws.evJoin); cudaEventDestroy(ws.evJoinC);
     }
-    CK(cudaStreamCreateWithFlags(&ws.sB, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&ws.sC, cudaStreamNonBlocking));
+    // Priorities: the critical path (window kernel -> critical strips -> next window kernel)
+    // runs on the highest-priority stream so that its CTAs are dispatched ahead of the queued
+    // update strips of the other streams (lowest priority).
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CK(cudaStreamCreateWithPriority(&ws.sH, cudaStreamNonBlocking, greatest));
+    CK(cudaStreamCreateWithPriority(&ws.sB, cudaStreamNonBlocking, least));
+    CK(cudaStreamCreateWithPriority(&ws.sC, cudaStreamNonBlocking, least));
+    CK(cudaEventCreateWithFlags(&ws.evIn, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ws.evOut, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&ws.sU, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ws.evQup, cudaEventDisableTiming));
     for (int i = 0; i < kZgen; ++i) {
@@ -210,11 +223,27 @@ namespace {
 
 // q_ready (optional): an event after which Q holds its input (a host upload still in flight
 // while the structure scan, the plan and the first levels' S updates run)
+int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ, int32_t* select,
+           int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA, cudaEvent_t q_ready);
+
+// The call is ordered on the caller's stream: the work runs on the library's streams between
+// an event recorded on it and a wait it gets at the end.
 int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ, int32_t* select,
-        int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA, cudaEvent_t q_ready = nullptr) {
+        int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sUser, cudaEvent_t q_ready = nullptr) {
+  Workspace& ws = g_ws;
+  if (int rc = ensure_runtime(ws)) return rc;
+  CK(cudaEventRecord(ws.evIn, sUser));
+  CK(cudaStreamWaitEvent(ws.sH, ws.evIn, 0));
+  const int rc = run_on(o, n, S, ldS, Q, ldQ, select, m, bmap_out, st, ws.sH, q_ready);
+  cudaEventRecord(ws.evOut, ws.sH);
+  cudaStreamWaitEvent(sUser, ws.evOut, 0);
+  return rc;
+}
+
+int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ, int32_t* select,
+           int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA, cudaEvent_t q_ready) {
   Workspace& ws = g_ws;
   const double t_start = now_ms();
-  if (int rc = ensure_runtime(ws)) return rc;
   int64_t launches[5] = {0, 0, 0, 0, 0};
   std::vector<std::pair<int, int>> prof_marks;   // (kind, first event index)
   size_t prof_used = 0;
