@@ -23,8 +23,7 @@ constexpr int LDD = 65;   // inner window (odd stride: conflict-free row walks)
 constexpr int LDZ = 68;   // inner accumulator (== 4 mod 16: conflict-free DMMA fragments)
 constexpr int LDT = 68;   // staging tile
 
-__device__ int g_wdbg;
-__device__ int g_tprof_on;   // debug timing switch (set with WindowArgs::tprof)   // debug: 1 skip phase B, 2 skip phase C (timing experiments only)
+__device__ int g_tprof_on;   // debug timing switch (set with WindowArgs::tprof)
 
 // block list of the window being processed (one CTA per window)
 __shared__ uint8_t g_bsz[256], g_bsel[256];
@@ -622,13 +621,6 @@ size_t window_smem_bytes() {
 
 void launch_window(const WindowArgs& a, cudaStream_t st) {
   static bool attr = false;
-  static const int wdbg = [] {
-    const char* e = std::getenv("SN_WDBG");
-    const int v = e ? std::atoi(e) : 0;
-    cudaMemcpyToSymbol(g_wdbg, &v, sizeof(int));
-    return v;
-  }();
-  (void)wdbg;
   static int tprof_state = -1;
   const int want = a.tprof ? 1 : 0;
   if (tprof_state != want) { cudaMemcpyToSymbol(g_tprof_on, &want, sizeof(int)); tprof_state = want; }
