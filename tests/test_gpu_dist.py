@@ -132,3 +132,26 @@ def test_dist_nccl_world1_matches_single():
         assert np.array_equal(S1, Sg2) and np.array_equal(Q1, Qg2)
     finally:
         sn.dist_finalize()
+
+
+def test_dist_local_config3_fullsize_bitwise():
+    """The sharded program at the bench size (config 3, n = 40 000, bc = 512) for 4 ranks on
+    one device: S and Q bitwise equal to the one-GPU executor (compared on the device)."""
+    from workloads import make_config
+    p = make_config(3, seed=1, device="cuda")
+    n, P, bc = p.n, 4, 512
+    shards = [sn.shard(p.S, p.Q, P, bc, r) for r in range(P)]
+    Sl = [s for s, _ in shards]
+    Ql = [q for _, q in shards]
+    del shards
+    g1 = sn.reorder(p.S, p.Q, p.select, window=p.w)
+    got = sn.reorder_dist_local(Sl, Ql, p.select, n, bc, window=p.w)
+    torch.cuda.synchronize()
+    assert g1["rc"] == 0 and got["rc"] == 0
+    np.testing.assert_array_equal(got["bmap"], g1["bmap"])
+    assert got["stats"]["windows"] == g1["stats"]["windows"]
+    for r in range(P):
+        cols = torch.as_tensor(sn.owned_columns(n, P, bc, r), device="cuda")
+        assert torch.equal(p.S[cols], Sl[r][:len(cols)])
+        _, q0, q1 = sn.dist_layout(n, P, bc, r)
+        assert torch.equal(p.Q[:, q0:q1], Ql[r][:, :q1 - q0])
