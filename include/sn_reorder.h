@@ -173,7 +173,10 @@ int sn_reorder_schur_dist_local(const sn_opts* opts, int64_t P, int64_t n, int64
  *   (1, level, t, j1, k, owner, partner, coff)                       window (level-sorted)
  *   (2, level, w0, w1, npull, nL, nR, nQ)                            level, then its
  *   (3, w, src, dst, nrows, ncols, src_lcol, dst_lcol)  pulls, (4, wl, cnt, x0, 0..) L strips,
- *   (5, ...) R strips, (7, ...) pushes, (6, ...) Q strips, in execution order.
+ *   (5, ...) R strips, (7, ...) pushes, (8, ...) remaining L strips, (9, ...) remaining R
+ *   strips, (6, ...) Q strips.  Execution order per level: pulls, window tasks, Z broadcast,
+ *   the previous level's remaining L then R strips, this level's (critical) L then R strips,
+ *   pushes; Q strips any time after the broadcast.
  * Local columns are in the extended layout: block lb at [lb*(bc+w), lb*(bc+w)+bc), its halo
  * slot after it. */
 int64_t sn_dist_program(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w, int64_t col_block, int64_t P,

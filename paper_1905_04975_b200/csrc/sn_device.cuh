@@ -32,8 +32,9 @@ struct WinDev {
   int32_t pad;
 };
 
-// One panel strip given explicitly (the sharded executor, sn_dist.h): window index within
-// the level, columns (left) or rows (right, Q), and the first column / row.
+// One panel segment given explicitly (the sharded executor, sn_dist.h): window index within
+// the level, columns (left) or rows (right, Q), and the first column / row.  A segment is
+// processed as ceil(cnt / 64) strips of 64.
 struct StripDev {
   int32_t w;
   int32_t cnt;
@@ -87,7 +88,9 @@ struct PanelArgs {
   int32_t nwin;
   int32_t base;
   const int32_t* prefix;    // nwin+1 cumulative strip counts of this kind and part
-  const StripDev* strips;   // explicit strips (sharded executor); prefix unused if set
+  const StripDev* strips;   // explicit segments (sharded executor): then prefix[0..nseg] holds
+                            // the strips before each segment
+  int32_t nseg;
   int32_t part;             // 0 all strips, 1 the critical strips, 2 the remaining strips
   int32_t vec16;            // M is 16-byte aligned and ld is even: 16-byte row-strip copies
   const int32_t* status;

@@ -16,6 +16,11 @@
 //   5 R      right update S[0:j1, j1:j2] <- S Z on the owner (contiguous via the halo slot)
 //   6 PUSH   owner -> partner, S[0:j2, c:j2] back from the halo slot
 //   7 Q      Q[:, j1:j2] <- Q Z on every rank, its own rows
+// Lookahead: steps 4-5 run only the *critical* strips before the push -- the strips the next
+// level's window tasks read, the strips on columns the next level pulls, the
+// halo strips and every right strip of a straddling window; the remaining strips run on a
+// second stream after the push, overlapping the next level's pulls and window tasks, and the
+// next level's updates wait for them.
 // The program is a pure function of (plan, n, P, bc, w, rank): identical on every rank,
 // so the collectives match by construction.  It is exported (sn_dist_program) so that the
 // CPU tests can interpret it with gloo (tests/test_dist_program.py).
@@ -83,7 +88,14 @@ struct DistLevel {
   int64_t w0 = 0, w1 = 0;                       // level-sorted window range
   std::vector<int64_t> pulls, pushes;           // indices into msgs
   std::vector<int64_t> own;                     // level-sorted indices owned by this rank
-  int64_t L0 = 0, L1 = 0, R0 = 0, R1 = 0, Q0 = 0, Q1 = 0;   // ranges in strips
+  // ranges in strips: critical left/right strips (before the push and the next level's
+  // pulls and window tasks), the remaining ones (overlapping the next level's window tasks),
+  // and the Q strips
+  int64_t L0 = 0, L1 = 0, R0 = 0, R1 = 0, Lr0 = 0, Lr1 = 0, Rr0 = 0, Rr1 = 0, Q0 = 0, Q1 = 0;
+  // per group (L, R, Lr, Rr, Q): offset of its strip prefix in DistProgram::sprefix (segments + 1
+  // entries) and its number of strips
+  int64_t poff[5] = {0, 0, 0, 0, 0};
+  int32_t nstr[5] = {0, 0, 0, 0, 0};
 };
 
 struct DistProgram {
@@ -92,7 +104,8 @@ struct DistProgram {
   std::vector<DistWin> wins;       // level-sorted (identical on every rank)
   std::vector<int64_t> sorted;     // level-sorted index -> schedule order
   std::vector<DistMsg> msgs;       // all ranks' messages
-  std::vector<DistStrip> strips;   // this rank's strips
+  std::vector<DistStrip> strips;   // this rank's segments (ranges of strips of `strip`)
+  std::vector<int32_t> sprefix;    // per group, strips before each segment (DistLevel::poff)
   std::vector<DistLevel> levels;
   int64_t max_level_wins = 0;
   int64_t max_msg_bytes = 0;       // largest per-level staging need of this rank (bytes)

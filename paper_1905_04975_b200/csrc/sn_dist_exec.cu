@@ -129,9 +129,10 @@ struct DBuf {
 
 struct DistWorkspace {
   DBuf wins, pool, status, ctl, Z, zr, sub, bad;
-  std::vector<DBuf> Sx, own, strips, stage;   // per local rank
-  cudaStream_t sB = nullptr;
-  cudaEvent_t evW[kZgenD] = {}, evQ[kZgenD] = {};
+  std::vector<DBuf> Sx, own, strips, spref, stage;   // per local rank
+  cudaStream_t sB = nullptr, sC = nullptr, sH = nullptr;   // Q / remaining strips / critical path
+  cudaEvent_t evW[kZgenD] = {}, evQ[kZgenD] = {}, evCrit[kZgenD] = {}, evRest[kZgenD] = {};
+  cudaEvent_t evIn = nullptr, evOut = nullptr, evJoinC = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evJoin = nullptr;
   int device = -1;
 };
@@ -141,11 +142,20 @@ int ensure_dist_runtime(DistWorkspace& ws, int64_t nlocal) {
   int dev = 0;
   DCK(cudaGetDevice(&dev));
   if (ws.device != dev) {
-    DCK(cudaStreamCreateWithFlags(&ws.sB, cudaStreamNonBlocking));
+    int least = 0, greatest = 0;
+    DCK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    DCK(cudaStreamCreateWithPriority(&ws.sH, cudaStreamNonBlocking, greatest));
+    DCK(cudaStreamCreateWithPriority(&ws.sB, cudaStreamNonBlocking, least));
+    DCK(cudaStreamCreateWithPriority(&ws.sC, cudaStreamNonBlocking, least));
     for (int i = 0; i < kZgenD; ++i) {
       DCK(cudaEventCreateWithFlags(&ws.evW[i], cudaEventDisableTiming));
       DCK(cudaEventCreateWithFlags(&ws.evQ[i], cudaEventDisableTiming));
+      DCK(cudaEventCreateWithFlags(&ws.evCrit[i], cudaEventDisableTiming));
+      DCK(cudaEventCreateWithFlags(&ws.evRest[i], cudaEventDisableTiming));
     }
+    DCK(cudaEventCreateWithFlags(&ws.evIn, cudaEventDisableTiming));
+    DCK(cudaEventCreateWithFlags(&ws.evOut, cudaEventDisableTiming));
+    DCK(cudaEventCreateWithFlags(&ws.evJoinC, cudaEventDisableTiming));
     DCK(cudaEventCreate(&ws.ev0));
     DCK(cudaEventCreate(&ws.ev1));
     DCK(cudaEventCreateWithFlags(&ws.evJoin, cudaEventDisableTiming));
@@ -155,6 +165,7 @@ int ensure_dist_runtime(DistWorkspace& ws, int64_t nlocal) {
     ws.Sx.resize(nlocal);
     ws.own.resize(nlocal);
     ws.strips.resize(nlocal);
+    ws.spref.resize(nlocal);
     ws.stage.resize(nlocal);
   }
   return 0;
@@ -173,6 +184,7 @@ struct RankRun {
   std::vector<int64_t> own_off;       // per level, offset into own
   WinDev* d_own = nullptr;
   StripDev* d_strips = nullptr;
+  int32_t* d_spref = nullptr;
   char* stage = nullptr;
 };
 
@@ -243,8 +255,27 @@ int exchange(const std::vector<RankRun>& rr, const DistProgram& prog0, const std
 
 // The sharded reordering.  io has one entry per local rank (NCCL: exactly one, rank =
 // g_comm.rank; local: P entries, rank = index).
+int run_dist_on(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, const std::vector<RankIO>& io,
+                int64_t ldu, int64_t ldq, int32_t* select, int64_t* m, int8_t* bmap_out, sn_stats* st,
+                cudaStream_t sA);
+
+// ordered on the caller's stream; the work runs on the library's high-priority stream
 int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, const std::vector<RankIO>& io,
-             int64_t ldu, int64_t ldq, int32_t* select, int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA) {
+             int64_t ldu, int64_t ldq, int32_t* select, int64_t* m, int8_t* bmap_out, sn_stats* st,
+             cudaStream_t sUser) {
+  DistWorkspace& ws = g_dws;
+  if (int rc = ensure_dist_runtime(ws, (int64_t)io.size())) return rc;
+  DCK(cudaEventRecord(ws.evIn, sUser));
+  DCK(cudaStreamWaitEvent(ws.sH, ws.evIn, 0));
+  const int rc = run_dist_on(o, n, bc, P, nccl, io, ldu, ldq, select, m, bmap_out, st, ws.sH);
+  cudaEventRecord(ws.evOut, ws.sH);
+  cudaStreamWaitEvent(sUser, ws.evOut, 0);
+  return rc;
+}
+
+int run_dist_on(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, const std::vector<RankIO>& io,
+                int64_t ldu, int64_t ldq, int32_t* select, int64_t* m, int8_t* bmap_out, sn_stats* st,
+                cudaStream_t sA) {
   DistWorkspace& ws = g_dws;
   const double t_start = now_ms();
   const int64_t nloc = (int64_t)io.size();
@@ -357,6 +388,11 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
     DCK(ws.strips[q].ensure(sizeof(StripDev) * std::max<size_t>(1, R.prog.strips.size())));
     R.d_own = (WinDev*)ws.own[q].p;
     R.d_strips = (StripDev*)ws.strips[q].p;
+    DCK(ws.spref[q].ensure(sizeof(int32_t) * std::max<size_t>(1, R.prog.sprefix.size())));
+    R.d_spref = (int32_t*)ws.spref[q].p;
+    if (!R.prog.sprefix.empty())
+      DCK(cudaMemcpyAsync(R.d_spref, R.prog.sprefix.data(), sizeof(int32_t) * R.prog.sprefix.size(),
+                          cudaMemcpyHostToDevice, sA));
     if (!R.own.empty())
       DCK(cudaMemcpyAsync(R.d_own, R.own.data(), sizeof(WinDev) * R.own.size(), cudaMemcpyHostToDevice, sA));
     if (!R.prog.strips.empty())
@@ -375,6 +411,8 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
   double* dZ = (double*)ws.Z.p;
   const bool overlapQ = o.q_stream_overlap != 0 && hasQ;
   cudaStream_t sQ = overlapQ ? ws.sB : sA;
+  const bool look = o.lookahead != 0;
+  cudaStream_t sC = ws.sC;
   std::vector<PanelMaps> mapS(nloc), mapQ(nloc);
   for (int64_t q = 0; q < nloc; ++q) {
     const int64_t r = rr[q].rank;
@@ -386,6 +424,7 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
   }
   DCK(cudaEventRecord(ws.ev0, sA));
   if (overlapQ) DCK(cudaStreamWaitEvent(ws.sB, ws.ev0, 0));
+  if (look) DCK(cudaStreamWaitEvent(sC, ws.ev0, 0));
 
   for (int64_t l = 0; l < nlev; ++l) {
     const DistLevel& LG = G.levels[l];
@@ -422,39 +461,61 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
       NCK(g_nccl.GroupEnd());
     }
     if (overlapQ) DCK(cudaEventRecord(ws.evW[gen], sA));
-    // 4 L, 5 R
-    for (int kind = 0; kind < 2; ++kind) {
+    // 4 L, 5 R: the critical strips on the critical path (after the previous level's
+    // remaining strips), the remaining strips on stream C after the push
+    if (look && l > 0) DCK(cudaStreamWaitEvent(sA, ws.evRest[(l - 1) % kZgenD], 0));
+    auto panels = [&](int kind, bool crit, cudaStream_t s) {
       for (int64_t q = 0; q < nloc; ++q) {
         RankRun& R = rr[q];
         const DistLevel& LR = R.prog.levels[l];
-        const int64_t s0 = kind == 0 ? LR.L0 : LR.R0, s1 = kind == 0 ? LR.L1 : LR.R1;
-        if (s1 <= s0) continue;
+        const int64_t s0 = kind == 0 ? (crit ? LR.L0 : LR.Lr0) : (crit ? LR.R0 : LR.Rr0);
+        const int64_t s1 = kind == 0 ? (crit ? LR.L1 : LR.Lr1) : (crit ? LR.R1 : LR.Rr1);
+        const int g = kind == 0 ? (crit ? 0 : 2) : (crit ? 1 : 3);
+        if (s1 <= s0 || LR.nstr[g] <= 0) continue;
         PanelArgs pa{};
         pa.wins = dw + w0; pa.nwin = (int32_t)cnt; pa.base = (int32_t)w0; pa.status = dstatus;
-        pa.strips = R.d_strips + s0; pa.prefix = nullptr; pa.part = 0;
+        pa.strips = R.d_strips + s0; pa.nseg = (int32_t)(s1 - s0); pa.prefix = R.d_spref + LR.poff[g];
+        pa.part = 0;
         pa.n = n; pa.Z = dZ; pa.zrange = dzr; pa.M = R.Sx; pa.ld = ldx; pa.maps = &mapS[q];
         pa.vec16 = ((uintptr_t)R.Sx % 16) == 0 ? 1 : 0;
-        launch_panel(kind, mt, pa, (int32_t)(s1 - s0), sA);
+        launch_panel(kind, mt, pa, LR.nstr[g], s);
         launches[1 + kind]++;
       }
+    };
+    panels(0, true, sA);
+    panels(1, true, sA);
+    if (!look) {
+      // one-stream order: the remaining strips of this level right after its critical ones
+      // (left before right on every corner, as in the one-GPU executor)
+      panels(0, false, sA);
+      panels(1, false, sA);
     }
     DCK(cudaGetLastError());
     // 6 PUSH
     if (int rc = exchange(rr, G, LG.pushes, ldx, nccl, sA)) return rc;
+    if (look) {
+      DCK(cudaEventRecord(ws.evCrit[gen], sA));
+      DCK(cudaStreamWaitEvent(sC, ws.evCrit[gen], 0));
+      panels(0, false, sC);
+      panels(1, false, sC);
+      DCK(cudaEventRecord(ws.evRest[gen], sC));
+      DCK(cudaGetLastError());
+    }
     // 7 Q
     if (hasQ) {
       if (overlapQ) DCK(cudaStreamWaitEvent(sQ, ws.evW[gen], 0));
       for (int64_t q = 0; q < nloc; ++q) {
         RankRun& R = rr[q];
         const DistLevel& LR = R.prog.levels[l];
-        if (LR.Q1 <= LR.Q0) continue;
+        if (LR.Q1 <= LR.Q0 || LR.nstr[4] <= 0) continue;
         PanelArgs pa{};
         pa.wins = dw + w0; pa.nwin = (int32_t)cnt; pa.base = (int32_t)w0; pa.status = dstatus;
-        pa.strips = R.d_strips + LR.Q0; pa.prefix = nullptr; pa.part = 0;
+        pa.strips = R.d_strips + LR.Q0; pa.nseg = (int32_t)(LR.Q1 - LR.Q0); pa.prefix = R.d_spref + LR.poff[4];
+        pa.part = 0;
         pa.n = lay.q1(R.rank) - lay.q0(R.rank); pa.Z = dZ; pa.zrange = dzr; pa.M = io[q].Q; pa.ld = ldq;
         pa.maps = &mapQ[q];
         pa.vec16 = (ldq % 2 == 0 && ((uintptr_t)io[q].Q % 16) == 0) ? 1 : 0;
-        launch_panel(2, mt, pa, (int32_t)(LR.Q1 - LR.Q0), sQ);
+        launch_panel(2, mt, pa, LR.nstr[4], sQ);
         launches[3]++;
       }
       DCK(cudaGetLastError());
@@ -468,6 +529,10 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
   if (overlapQ) {
     DCK(cudaEventRecord(ws.evJoin, sQ));
     DCK(cudaStreamWaitEvent(sA, ws.evJoin, 0));
+  }
+  if (look) {
+    DCK(cudaEventRecord(ws.evJoinC, sC));
+    DCK(cudaStreamWaitEvent(sA, ws.evJoinC, 0));
   }
   DCK(cudaEventRecord(ws.ev1, sA));
   Control ctl;
@@ -731,6 +796,8 @@ int64_t sn_dist_program(int64_t n, const int8_t* bmap, const int8_t* selrow, int
       const sn::DistMsg& m = D.msgs[mi];
       put(7, m.w, m.src, m.dst, m.nrows, m.ncols, m.src_lcol, m.dst_lcol);
     }
+    for (int64_t q = L.Lr0; q < L.Lr1; ++q) put(8, D.strips[q].w, D.strips[q].cnt, D.strips[q].x0, 0, 0, 0, 0);
+    for (int64_t q = L.Rr0; q < L.Rr1; ++q) put(9, D.strips[q].w, D.strips[q].cnt, D.strips[q].x0, 0, 0, 0, 0);
     for (int64_t s = L.Q0; s < L.Q1; ++s) put(6, D.strips[s].w, D.strips[s].cnt, D.strips[s].x0, 0, 0, 0, 0);
   }
   return cnt;

@@ -73,11 +73,18 @@ __global__ void __launch_bounds__(THREADS, 1) panel_kernel(PanelArgs a) {
   int w, nx;       // window index within the level; valid columns (left) or rows (right/Q)
   int64_t x0;      // first column (left) or row (right/Q) of the strip
   if (a.strips) {
-    // explicit strip (sharded executor, sn_dist.h)
-    const StripDev sd = a.strips[blockIdx.x];
+    // explicit segments (sharded executor, sn_dist.h)
+    const int sid = blockIdx.x;
+    int lo = 0, hi = a.nseg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.prefix[mid] <= sid) lo = mid; else hi = mid - 1;
+    }
+    const StripDev sd = a.strips[lo];
+    const int idx = sid - a.prefix[lo];
     w = sd.w;
-    x0 = sd.x0;
-    nx = sd.cnt;
+    x0 = sd.x0 + (int64_t)idx * NT;
+    nx = min(NT, sd.cnt - idx * NT);
   } else {
     // strip -> (window, index) by binary search over the level's prefix
     const int sid = blockIdx.x;

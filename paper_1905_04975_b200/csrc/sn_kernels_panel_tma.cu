@@ -106,10 +106,16 @@ __device__ __forceinline__ StripInfo resolve(const PanelArgs& a, int sid) {
   StripInfo s;
   int w;
   if (a.strips) {
-    const StripDev sd = a.strips[sid];
+    int lo = 0, hi = a.nseg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.prefix[mid] <= sid) lo = mid; else hi = mid - 1;
+    }
+    const StripDev sd = a.strips[lo];
+    const int idx = sid - a.prefix[lo];
     w = sd.w;
-    s.x0 = sd.x0;
-    s.nx = sd.cnt;
+    s.x0 = sd.x0 + (int64_t)idx * NT;
+    s.nx = min(NT, sd.cnt - idx * NT);
   } else {
     int lo = 0, hi = a.nwin - 1;
     while (lo < hi) {

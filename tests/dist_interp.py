@@ -31,9 +31,10 @@ def parse(rec):
     for _ in range(nlev):
         r = rec[i]
         assert r[0] == 2
-        lev = dict(level=int(r[1]), w0=int(r[2]), w1=int(r[3]), pull=[], L=[], R=[], push=[], Q=[])
+        lev = dict(level=int(r[1]), w0=int(r[2]), w1=int(r[3]), pull=[], L=[], R=[], push=[], Q=[],
+                   Lr=[], Rr=[])
         i += 1
-        key = {3: "pull", 4: "L", 5: "R", 7: "push", 6: "Q"}
+        key = {3: "pull", 4: "L", 5: "R", 7: "push", 6: "Q", 8: "Lr", 9: "Rr"}
         while i < len(rec) and rec[i, 0] != 2:
             lev[key[int(rec[i, 0])]].append(tuple(int(x) for x in rec[i, 1:]))
             i += 1
@@ -94,17 +95,17 @@ def do_W(me, lev, wins, Zs, sched, rank):
         Zs[i] = Z
 
 
-def do_L(me, lev, wins, Zs):
+def do_L(me, lev, wins, Zs, key="L"):
     Sx, w0 = me["Sx"], lev["w0"]
-    for (wl, cnt, x0, *_r) in lev["L"]:
+    for (wl, cnt, x0, *_r) in lev[key]:
         w = wins[w0 + wl]
         j1, k = w["j1"], w["k"]
         Sx[j1:j1 + k, x0:x0 + cnt] = Zs[w0 + wl].T @ Sx[j1:j1 + k, x0:x0 + cnt]
 
 
-def do_R(me, lev, wins, Zs, rank):
+def do_R(me, lev, wins, Zs, rank, key="R"):
     Sx, w0 = me["Sx"], lev["w0"]
-    for (wl, cnt, x0, *_r) in lev["R"]:
+    for (wl, cnt, x0, *_r) in lev[key]:
         w = wins[w0 + wl]
         j1, k, c = w["j1"], w["k"], w["coff"]
         assert w["owner"] == rank
@@ -150,13 +151,20 @@ def run_shared(S, Q, select, w, bc, P):
     Zs = {}
     sh = Shared(states)
     nlev = progs[0][0]["nlev"]
+    prev = None
     for l in range(nlev):
-        # phase by phase over the ranks, as sn_reorder_schur_dist_local executes
+        # phase by phase over the ranks, in the executor's order: the previous level's
+        # remaining strips run only after this level's pulls and window tasks
         levs = [progs[r][2][l] for r in range(P)]
         for m in levs[0]["pull"]:
             sh.send(m[1], m[2], m[3], m[4], m[5], m[6])
         for r in range(P):
             do_W(states[r], levs[r], progs[r][1], Zs, sched, r)
+        if prev is not None:
+            for r in range(P):
+                do_L(states[r], prev[r], progs[r][1], Zs, "Lr")
+            for r in range(P):
+                do_R(states[r], prev[r], progs[r][1], Zs, r, "Rr")
         for r in range(P):
             do_L(states[r], levs[r], progs[r][1], Zs)
         for r in range(P):
@@ -165,6 +173,12 @@ def run_shared(S, Q, select, w, bc, P):
             sh.send(m[1], m[2], m[3], m[4], m[5], m[6])
         for r in range(P):
             do_Q(states[r], levs[r], progs[r][1], Zs)
+        prev = levs
+    if prev is not None:
+        for r in range(P):
+            do_L(states[r], prev[r], progs[r][1], Zs, "Lr")
+        for r in range(P):
+            do_R(states[r], prev[r], progs[r][1], Zs, r, "Rr")
     Sg = gather(states, n, P, bc, w)
     Qg = None
     if Q is not None:
@@ -204,6 +218,7 @@ def run_gloo(S, Q, select, w, bc, rank, P):
                 nrows, ncols, dl = meta
                 Sx[:nrows, dl:dl + ncols] = t.numpy()
 
+    prev = None
     for lev in levels:
         exchange(lev["pull"])
         do_W(me, lev, wins, Zs, sched, rank)
@@ -213,8 +228,15 @@ def run_gloo(S, Q, select, w, bc, rank, P):
                 torch.empty((k, k), dtype=torch.float64)
             dist.broadcast(t, src=wins[i]["owner"])
             Zs[i] = t.numpy()
+        if prev is not None:
+            do_L(me, prev, wins, Zs, "Lr")
+            do_R(me, prev, wins, Zs, rank, "Rr")
         do_L(me, lev, wins, Zs)
         do_R(me, lev, wins, Zs, rank)
         exchange(lev["push"])
         do_Q(me, lev, wins, Zs)
+        prev = lev
+    if prev is not None:
+        do_L(me, prev, wins, Zs, "Lr")
+        do_R(me, prev, wins, Zs, rank, "Rr")
     return me, hdr

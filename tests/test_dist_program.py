@@ -79,7 +79,7 @@ def test_program_structure():
         for r in range(P):
             # R strips only on the owner, covering rows [0, j1) exactly once
             rows = {}
-            for (wl, cnt, x0, *_z) in progs[r][2][l]["R"]:
+            for (wl, cnt, x0, *_z) in progs[r][2][l]["R"] + progs[r][2][l]["Rr"]:
                 assert wins0[lev["w0"] + wl]["owner"] == r
                 rows.setdefault(wl, []).append((x0, cnt))
             for wl, segs in rows.items():
@@ -101,7 +101,7 @@ def test_program_structure():
                         c = (y["j1"] // bc + 1) * bc
                         for j in range(c, y["j1"] + y["k"]):
                             inv[DI.ext_lcol(y["j1"], P, bc, w) + (j - y["j1"])] = j
-                for (wl, cnt, x0, *_z) in progs[r][2][l]["L"]:
+                for (wl, cnt, x0, *_z) in progs[r][2][l]["L"] + progs[r][2][l]["Lr"]:
                     if lev["w0"] + wl != i:
                         continue
                     for lc in range(x0, x0 + cnt):
