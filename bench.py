@@ -287,7 +287,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--oracle-gflop", type=float, default=40.0, help="size of the oracle sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--col-block", type=int, default=512, help="column block width of the sharded S")
+    ap.add_argument("--col-block", type=int, default=1024, help="column block width of the sharded S")
     ap.add_argument("--emulate-ranks", type=int, default=0, help="sharded program for P ranks on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
