@@ -18,7 +18,9 @@
  * Conventions for every entry point:
  *   - matrices are FP64, column-major, element (i,j) at a[i + j*ld], 0-based;
  *   - S and Q may be DEVICE pointers (cudaMalloc / torch CUDA tensors: the fast path) or
- *     HOST pointers (pageable or pinned; staged through device memory inside the call);
+ *     HOST pointers (pageable or pinned; staged through device memory inside the call: Q is
+ *     uploaded while the first levels run, and the final columns of S and Q are copied back
+ *     as they become final; the staging memory is kept, see sn_release_workspace);
  *   - the caller owns every buffer; S and Q are modified in place (LAPACK style);
  *   - `select` is a HOST int32 array of n entries, one per row: nonzero = selected.  A
  *     2x2 block is selected if either of its rows is (LAPACK DTRSEN convention).
@@ -181,6 +183,10 @@ int sn_reorder_schur_dist_local(const sn_opts* opts, int64_t P, int64_t n, int64
  * slot after it. */
 int64_t sn_dist_program(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w, int64_t col_block, int64_t P,
                         int64_t rank, int64_t cap, int64_t* rec);
+
+/* Frees the device workspace the one-GPU entry points keep between calls (descriptors, Z
+ * slots and, after host-buffer calls, the 2 n^2 doubles that stage S and Q). */
+void sn_release_workspace(void);
 
 /* Library version string. */
 const char* sn_version(void);

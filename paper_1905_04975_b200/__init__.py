@@ -75,7 +75,7 @@ SN_OK, SN_ERR_REJECTED, SN_ERR_CUDA, SN_ERR_NCCL, SN_ERR_UNSUPPORTED = 0, 1, 2, 
 EXPORTS = ["sn_default_opts", "sn_strerror", "sn_reorder_schur", "sn_reorder_schur_ex",
            "sn_schedule_build", "sn_schedule_lookahead", "sn_schedule_window_swaps", "sn_version",
            "sn_dist_unique_id", "sn_dist_init", "sn_dist_finalize", "sn_dist_layout", "sn_reorder_schur_dist",
-           "sn_reorder_schur_dist_local", "sn_dist_program"]
+           "sn_reorder_schur_dist_local", "sn_dist_program", "sn_release_workspace"]
 
 _lib = None
 

@@ -49,9 +49,12 @@ struct DevBuf {
 
 struct Workspace {
   DevBuf wins, pool, prefix, status, kwork, ctl, Z, zr, sub, bad;
+  DevBuf hS, hQ;                   // device staging of host-buffer calls (kept between calls)
   std::vector<cudaEvent_t> prof;   // event pool for opts.profile
   cudaStream_t sB = nullptr, sC = nullptr, sU = nullptr;   // sU: host->device upload of Q
   cudaStream_t sH = nullptr;      // high priority: window tasks and the strips they wait for
+  cudaStream_t sD = nullptr;      // device -> host copies of final columns (host-buffer calls)
+  std::vector<cudaEvent_t> evPool;
   cudaEvent_t evIn = nullptr, evOut = nullptr;
   cudaEvent_t evQup = nullptr;
   cudaEvent_t evW[kZgen] = {}, evQ[kZgen] = {}, evCrit[kZgen] = {}, evRest[kZgen] = {};
@@ -89,6 +92,9 @@ int ensure_runtime(Workspace& ws) {
       cudaStreamDestroy(ws.sC);
       cudaStreamDestroy(ws.sH);
       cudaStreamDestroy(ws.sU);
+      cudaStreamDestroy(ws.sD);
+      for (auto e : ws.evPool) cudaEventDestroy(e);
+      ws.evPool.clear();
       cudaEventDestroy(ws.evIn); cudaEventDestroy(ws.evOut); cudaEventDestroy(ws.evQup);
       for (int i = 0; i < kZgen; ++i) {
         cudaEventDestroy(ws.evW[i]); cudaEventDestroy(ws.evQ[i]);
@@ -107,6 +113,7 @@ int ensure_runtime(Workspace& ws) {
     CK(cudaStreamCreateWithPriority(&ws.sC, cudaStreamNonBlocking, least));
     CK(cudaEventCreateWithFlags(&ws.evIn, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ws.evOut, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithPriority(&ws.sD, cudaStreamNonBlocking, least));
     CK(cudaStreamCreateWithFlags(&ws.sU, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ws.evQup, cudaEventDisableTiming));
     for (int i = 0; i < kZgen; ++i) {
@@ -221,27 +228,39 @@ void write_blocks(const std::vector<uint8_t>& fsz, const std::vector<uint8_t>& f
 
 namespace {
 
+// Host-buffer calls: the host copies of S and Q, filled column block by column block as the
+// columns become final (columns left of every later window's first row are never touched
+// again: later windows, their panels and their Q columns all lie at or right of their j1).
+struct HostOut {
+  double* S;
+  int64_t ldS;
+  double* Q;
+  int64_t ldQ;
+  int64_t copied;   // columns [0, copied) are on their way to the host
+};
+
 // q_ready (optional): an event after which Q holds its input (a host upload still in flight
 // while the structure scan, the plan and the first levels' S updates run)
 int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ, int32_t* select,
-           int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA, cudaEvent_t q_ready);
+           int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA, cudaEvent_t q_ready, HostOut* ho);
 
 // The call is ordered on the caller's stream: the work runs on the library's streams between
 // an event recorded on it and a wait it gets at the end.
 int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ, int32_t* select,
-        int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sUser, cudaEvent_t q_ready = nullptr) {
+        int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sUser, cudaEvent_t q_ready = nullptr,
+        HostOut* ho = nullptr) {
   Workspace& ws = g_ws;
   if (int rc = ensure_runtime(ws)) return rc;
   CK(cudaEventRecord(ws.evIn, sUser));
   CK(cudaStreamWaitEvent(ws.sH, ws.evIn, 0));
-  const int rc = run_on(o, n, S, ldS, Q, ldQ, select, m, bmap_out, st, ws.sH, q_ready);
+  const int rc = run_on(o, n, S, ldS, Q, ldQ, select, m, bmap_out, st, ws.sH, q_ready, ho);
   cudaEventRecord(ws.evOut, ws.sH);
   cudaStreamWaitEvent(sUser, ws.evOut, 0);
   return rc;
 }
 
 int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ, int32_t* select,
-           int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA, cudaEvent_t q_ready) {
+           int64_t* m, int8_t* bmap_out, sn_stats* st, cudaStream_t sA, cudaEvent_t q_ready, HostOut* ho) {
   Workspace& ws = g_ws;
   const double t_start = now_ms();
   int64_t launches[5] = {0, 0, 0, 0, 0};
@@ -393,6 +412,22 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
     CK(cudaMalloc(&dtp, 16 * sizeof(unsigned long long)));
     CK(cudaMemsetAsync(dtp, 0, 16 * sizeof(unsigned long long), sA));
   }
+  // final-column frontier after each level: the smallest first row of any later window
+  std::vector<int64_t> frontier(P.nlevels, n);
+  for (int64_t l = P.nlevels - 2; l >= 0; --l) {
+    int64_t mn = frontier[l + 1];
+    for (int64_t i = lstart[l + 1]; i < lstart[l + 2]; ++i) mn = std::min(mn, P.wins[sorted[i]].j1);
+    frontier[l] = mn;
+  }
+  size_t evUsed = 0;
+  auto next_event = [&]() -> cudaEvent_t {
+    if (evUsed == ws.evPool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+      ws.evPool.push_back(e);
+    }
+    return ws.evPool[evUsed++];
+  };
   CK(cudaEventRecord(ws.ev0, sA));
   if (overlapQ) {
     CK(cudaStreamWaitEvent(ws.sB, ws.ev0, 0));
@@ -462,6 +497,22 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
       CK(cudaStreamSynchronize(sA));
       if (overlapQ) CK(cudaStreamSynchronize(sQ));
       if (look) CK(cudaStreamSynchronize(sC));
+    }
+    // host-buffer call: columns [copied, frontier) are final once this level's work is done
+    if (ho && frontier[l] - ho->copied >= 2048 && l + 1 < P.nlevels) {
+      cudaEvent_t ea = next_event();
+      if (!ea) return SN_ERR_CUDA;
+      CK(cudaEventRecord(ea, sA));
+      CK(cudaStreamWaitEvent(ws.sD, ea, 0));
+      if (overlapQ) CK(cudaStreamWaitEvent(ws.sD, ws.evQ[gen], 0));
+      if (look) CK(cudaStreamWaitEvent(ws.sD, ws.evRest[gen], 0));
+      const int64_t c0 = ho->copied, nc = frontier[l] - c0;
+      CK(cudaMemcpy2DAsync(ho->S + c0 * ho->ldS, ho->ldS * 8, S + c0 * ldS, ldS * 8, n * 8, nc,
+                           cudaMemcpyDeviceToHost, ws.sD));
+      if (Q && ho->Q)
+        CK(cudaMemcpy2DAsync(ho->Q + c0 * ho->ldQ, ho->ldQ * 8, Q + c0 * ldQ, ldQ * 8, n * 8, nc,
+                             cudaMemcpyDeviceToHost, ws.sD));
+      ho->copied = frontier[l];
     }
   }
   if (overlapQ) {
@@ -589,6 +640,17 @@ const char* sn_strerror(int code) {
 
 const char* sn_version(void) { return "sn_b200 0.1 (sm_100a)"; }
 
+void sn_release_workspace(void) {
+  std::lock_guard<std::mutex> lock(sn::g_mu);
+  sn::Workspace& ws = sn::g_ws;
+  for (sn::DevBuf* b : {&ws.wins, &ws.pool, &ws.prefix, &ws.status, &ws.kwork, &ws.ctl, &ws.Z, &ws.zr, &ws.sub,
+                        &ws.bad, &ws.hS, &ws.hQ}) {
+    if (b->p) cudaFree(b->p);
+    b->p = nullptr;
+    b->cap = 0;
+  }
+}
+
 int sn_reorder_schur_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS, double* Q, int64_t ldQ,
                         int32_t* select, int64_t* m, int8_t* bmap_out, sn_stats* stats, void* stream) {
   sn_opts o;
@@ -623,10 +685,11 @@ int sn_reorder_schur_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS, 
   // scan, the plan and the first levels' S work run -- the Q updates wait for it.
   const double t0 = sn::now_ms();
   if (int rc = sn::ensure_runtime(sn::g_ws)) return rc;
-  double *dS = nullptr, *dQ = nullptr;
   const size_t bytes = sizeof(double) * (size_t)n * (size_t)n;
-  if (cudaMalloc(&dS, bytes) != cudaSuccess) return SN_ERR_CUDA;
-  if (Q && cudaMalloc(&dQ, bytes) != cudaSuccess) { cudaFree(dS); return SN_ERR_CUDA; }
+  if (sn::g_ws.hS.ensure(bytes) != cudaSuccess) return SN_ERR_CUDA;
+  if (Q && sn::g_ws.hQ.ensure(bytes) != cudaSuccess) return SN_ERR_CUDA;
+  double* dS = (double*)sn::g_ws.hS.p;
+  double* dQ = Q ? (double*)sn::g_ws.hQ.p : nullptr;
   auto copy = [&](double* dst, int64_t ldd, const double* src, int64_t lds, cudaMemcpyKind kind, cudaStream_t s) {
     if (ldd == n && lds == n) return cudaMemcpyAsync(dst, src, bytes, kind, s);   // one contiguous copy
     return cudaMemcpy2DAsync(dst, ldd * 8, src, lds * 8, n * 8, n, kind, s);
@@ -639,18 +702,22 @@ int sn_reorder_schur_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS, 
        cudaEventRecord(sn::g_ws.evQup, sU) != cudaSuccess))
     rc = SN_ERR_CUDA;
   const double t1 = sn::now_ms();
-  if (rc == SN_OK) rc = sn::run(o, n, dS, n, dQ, n, select, m, bmap_out, stats, sA, Q ? sn::g_ws.evQup : nullptr);
+  sn::HostOut ho{S, ldS, Q, ldQ, 0};
+  if (rc == SN_OK)
+    rc = sn::run(o, n, dS, n, dQ, n, select, m, bmap_out, stats, sA, Q ? sn::g_ws.evQup : nullptr, &ho);
   if (Q) cudaStreamSynchronize(sU);
   const double t2 = sn::now_ms();
   if (rc == SN_OK || rc == SN_ERR_REJECTED) {
-    if (copy(S, ldS, dS, n, cudaMemcpyDeviceToHost, sA) != cudaSuccess ||
-        (Q && copy(Q, ldQ, dQ, n, cudaMemcpyDeviceToHost, sA) != cudaSuccess) ||
-        cudaStreamSynchronize(sA) != cudaSuccess)
+    // the columns not streamed out during the run
+    const int64_t c0 = ho.copied, nc = n - c0;
+    if (nc > 0 &&
+        (cudaMemcpy2DAsync(S + c0 * ldS, ldS * 8, dS + c0 * n, n * 8, n * 8, nc, cudaMemcpyDeviceToHost, sA) != cudaSuccess ||
+         (Q && cudaMemcpy2DAsync(Q + c0 * ldQ, ldQ * 8, dQ + c0 * n, n * 8, n * 8, nc, cudaMemcpyDeviceToHost, sA) != cudaSuccess)))
       rc = SN_ERR_CUDA;
+    if (cudaStreamSynchronize(sA) != cudaSuccess) rc = SN_ERR_CUDA;
   }
+  if (cudaStreamSynchronize(sn::g_ws.sD) != cudaSuccess) rc = SN_ERR_CUDA;
   const double t3 = sn::now_ms();
-  cudaFree(dS);
-  if (dQ) cudaFree(dQ);
   if (stats) {
     stats->ms_h2d = t1 - t0;     // issue time of the uploads (they overlap the run)
     stats->ms_d2h = t3 - t2;
