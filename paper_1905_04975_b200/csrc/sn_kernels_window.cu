@@ -236,7 +236,7 @@ __device__ __forceinline__ int wave_assemble(int t, int j, int pv, const double*
     double x[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) x[c] = c < pnd ? Din[(j + r) + (jp + c) * LDD] : 0.0;
-    dev::rec_apply_row_t(pt, x, prec);
+    dev::rec_apply_generic(x, prec);
 #pragma unroll
     for (int c = 0; c < 4; ++c) cpl[r][c] = x[c];
 #pragma unroll
@@ -278,7 +278,11 @@ __device__ __forceinline__ void wave_transform_one(int t, int base, int lane, do
     wave_writeback<N1>(jp, pnd, j, Din, cpl);
   const long long q1 = g_tprof_on ? clock64() : 0;
   bool rj = force_here && (base + flat == force_swap);
-  if (!rj) rj = dev::swap_compute_blk<N1, N2>(Db, rec_t + (ty * 32 + lane) * dev::kRec);
+  if (!rj) {
+    double* rec = rec_t + (ty * 32 + lane) * dev::kRec;
+    rj = dev::swap_compute_blk<N1, N2>(Db, rec);
+    dev::rec_generic(ty, rec);
+  }
   if (g_tprof_on) {
     atomicMax(&W.tmax[2], (unsigned long long)(q1 - q0));
     atomicMax(&W.tmax[3], (unsigned long long)(clock64() - q1));
@@ -311,7 +315,7 @@ __device__ void wave_transform(int t, int base, double* Din, double* recs, WaveS
       const int nw = wave_assemble<2, 2>(t, j, W.lprev[sb][3][sl], Din, recs, Db, cpl, jp, pnd);
       __syncwarp();   // every lane has read the coupling rows before they are written back
       if (act && role == 0 && nw) wave_writeback<2>(jp, pnd, j, Din, cpl);
-      double tmp[dev::kRec];
+      double tmp[dev::kGen];
       const long long q1 = g_tprof_on ? clock64() : 0;
       bool rj = dev::swap_compute_22_paired_blk(Db, tmp, role);
       if (g_tprof_on) atomicMax(&W.tmax[3], (unsigned long long)(clock64() - q1));
@@ -319,7 +323,8 @@ __device__ void wave_transform(int t, int base, double* Din, double* recs, WaveS
         rj = rj || (force_here && (base + flat == force_swap));
         double* dst = rec_t + (3 * 32 + slot) * dev::kRec;
 #pragma unroll
-        for (int q = 0; q < dev::kRec; ++q) dst[q] = tmp[q];
+        for (int q = 0; q < dev::kGen; ++q) dst[q] = tmp[q];
+        dev::rec_generic(3, dst);
         W.frej[sb][flat] = rj ? 1 : 0;
         if (rj) atomicOr(&W.anyrej[sb], 1);
       }
