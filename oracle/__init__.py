@@ -64,6 +64,13 @@ def lib():
         _lib.or_reorder.argtypes = [i32, i64, p, i64, p, i64, p, C.POINTER(C.c_int64), i64, i64, i64,
                                     p, C.POINTER(Stats)]
         _lib.or_reorder.restype = i32
+        _lib.or_gsylv.argtypes = [i32, i32, p, p, p, p, p, p, p, p]
+        _lib.or_gsylv.restype = i32
+        _lib.or_gswap.argtypes = [i64, p, i64, p, i64, i64, i32, i32, p, i64, i64, p, i64, i64]
+        _lib.or_gswap.restype = i32
+        _lib.or_greorder.argtypes = [i32, i64, p, i64, p, i64, p, i64, p, i64, p, C.POINTER(C.c_int64),
+                                     i64, i64, i64, p, C.POINTER(Stats)]
+        _lib.or_greorder.restype = i32
     return _lib
 
 
@@ -178,3 +185,55 @@ def reorder(S, Q, select_rows, w: int, mode: int = 1, max_windows: int = -1,
     stats = {f: getattr(st, f) for f, _ in Stats._fields_}
     stats["swaps_by_type"] = list(st.swaps_by_type)
     return {"rc": rc, "S": Sx, "Q": Qx, "select": sel, "m": m.value, "bmap": bmap, "stats": stats}
+
+
+# ---- generalized reordering (sn_oracle.h) ---------------------------
+
+def _pad2(a, r, c):
+    out = np.zeros((2, 2), order="F")
+    out[:r, :c] = np.asarray(a, float).reshape(r, c)
+    return out
+
+
+def gsylv(A11, A22, A12, B11, B22, B12):
+    """Solve A11 R - L A22 = A12, B11 R - L B22 = B12; returns (R, L, perturbed)."""
+    A11 = np.atleast_2d(np.asarray(A11, float)); A22 = np.atleast_2d(np.asarray(A22, float))
+    n1, n2 = A11.shape[0], A22.shape[0]
+    args = [_pad2(A11, n1, n1), _pad2(A22, n2, n2), _pad2(A12, n1, n2),
+            _pad2(B11, n1, n1), _pad2(B22, n2, n2), _pad2(B12, n1, n2)]
+    R = np.zeros((2, 2), order="F"); L = np.zeros((2, 2), order="F")
+    info = lib().or_gsylv(n1, n2, *[_ptr(a) for a in args], _ptr(R), _ptr(L))
+    return R[:n1, :n2].copy(), L[:n1, :n2].copy(), info
+
+
+def gswap(S, T, j: int, n1: int, n2: int, Ql=None, Zr=None):
+    """Swap adjacent blocks of the pencil (S, T) on copies; returns (rc, S', T', Ql', Zr')."""
+    S = _f64(S).copy(order="F"); T = _f64(T).copy(order="F")
+    Qc = None if Ql is None else _f64(Ql).copy(order="F")
+    Zc = None if Zr is None else _f64(Zr).copy(order="F")
+    n = S.shape[0]
+    rc = lib().or_gswap(n, _ptr(S), n, _ptr(T), n, j, n1, n2,
+                        _ptr(Qc), 0 if Qc is None else Qc.shape[0], 0 if Qc is None else Qc.shape[0],
+                        _ptr(Zc), 0 if Zc is None else Zc.shape[0], 0 if Zc is None else Zc.shape[0])
+    return rc, S, T, Qc, Zc
+
+
+def greorder(S, T, Q, Z, select_rows, w: int, mode: int = 1, max_windows: int = -1,
+             force_reject_at: int = -1):
+    """Generalized reordering (Eq. (7) right form).  Returns dict(rc, S, T, Q, Z, select, m,
+    bmap, stats); all matrices Fortran fp64 copies."""
+    Sx = _f64(S).copy(order="F"); Tx = _f64(T).copy(order="F")
+    Qx = None if Q is None else _f64(Q).copy(order="F")
+    Zx = None if Z is None else _f64(Z).copy(order="F")
+    n = Sx.shape[0]
+    sel = np.ascontiguousarray(select_rows, np.int32).copy()
+    m = C.c_int64()
+    bmap = np.zeros(n, np.int8)
+    st = Stats()
+    ld = max(n, 1)
+    rc = lib().or_greorder(mode, n, _ptr(Sx), ld, _ptr(Tx), ld, _ptr(Qx), ld, _ptr(Zx), ld, _ptr(sel),
+                           C.byref(m), w, max_windows, force_reject_at, _ptr(bmap), C.byref(st))
+    stats = {f: getattr(st, f) for f, _ in Stats._fields_}
+    stats["swaps_by_type"] = list(st.swaps_by_type)
+    return {"rc": rc, "S": Sx, "T": Tx, "Q": Qx, "Z": Zx, "select": sel, "m": m.value, "bmap": bmap,
+            "stats": stats}

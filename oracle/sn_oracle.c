@@ -598,6 +598,26 @@ static int64_t sched_next(sched_t* st, int64_t* j1, int64_t* j2,
   }
 }
 
+/* Roll the block list back to the state reached in a window whose swap `done` was
+ * rejected: undo the swaps done..k-1 that sched_next performed symbolically. */
+static void sched_rollback(sched_t* st, const int64_t* tj, int64_t k, int64_t done) {
+  sched_t sc = *st;
+  for (int64_t i = k - 1; i >= done; --i) {
+    /* the swap exchanged blocks at rows tj[i] (size t1) and tj[i]+t1 (size t2);
+     * after it the block of size t2 is at row tj[i].  Find its index. */
+    int64_t lo = 0, hi = sc.B - 1, b = -1;
+    while (lo <= hi) {
+      int64_t mid = (lo + hi) / 2;
+      if (sc.brow[mid] == tj[i]) { b = mid; break; }
+      if (sc.brow[mid] < tj[i]) lo = mid + 1; else hi = mid - 1;
+    }
+    int8_t tsz = sc.bsz[b], tsel = sc.bsel[b];
+    sc.bsz[b] = sc.bsz[b + 1]; sc.bsel[b] = sc.bsel[b + 1];
+    sc.bsz[b + 1] = tsz; sc.bsel[b + 1] = tsel;
+    sc.brow[b + 1] = sc.brow[b] + sc.bsz[b];
+  }
+}
+
 /* Upper bound on the swaps of one window: a mover passes each other block at most once. */
 static int64_t max_swaps_per_window(int64_t w) { return (w * w) / 4 + w + 4; }
 
@@ -737,22 +757,7 @@ int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t l
       st->rejected_row = tj[done];
       st->rejected_n1 = t1[done];
       st->rejected_n2 = t2[done];
-      /* roll the block list back to the state reached: undo the swaps of this
-       * window that sched_next performed symbolically but were not executed */
-      for (int64_t i = k - 1; i >= done; --i) {
-        /* the swap exchanged blocks at rows tj[i] (size t1) and tj[i]+t1 (size t2);
-         * after it the block of size t2 is at row tj[i].  Find its index. */
-        int64_t lo = 0, hi = sc.B - 1, b = -1;
-        while (lo <= hi) {
-          int64_t mid = (lo + hi) / 2;
-          if (sc.brow[mid] == tj[i]) { b = mid; break; }
-          if (sc.brow[mid] < tj[i]) lo = mid + 1; else hi = mid - 1;
-        }
-        int8_t tsz = sc.bsz[b], tsel = sc.bsel[b];
-        sc.bsz[b] = sc.bsz[b + 1]; sc.bsel[b] = sc.bsel[b + 1];
-        sc.bsz[b + 1] = tsz; sc.bsel[b + 1] = tsel;
-        sc.brow[b + 1] = sc.brow[b] + sc.bsz[b];
-      }
+      sched_rollback(&sc, tj, k, done);
       break;
     }
     gswap += k;
@@ -766,6 +771,497 @@ int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t l
     }
   }
   free(tj); free(t1); free(t2); free(D); free(Z);
+  free(bmap); free(selrow);
+  sched_free(&sc);
+  return rc;
+}
+
+/* ===========================================================================
+ * Generalized reordering.  PAPER.md Eq. (7), right form
+ * (P:84-88): (S, T) = Q3 (Ŝ, T̂) Z3^T with Q3, Z3 orthogonal, the selected
+ * generalized eigenvalues moved to the leading diagonal blocks of (Ŝ, T̂);
+ * Table 1 lists it beside the standard case, on the same windowed
+ * machinery.  The paper gives no swap primitive for
+ * a pencil; restated here is the direct swapping method for generalized
+ * real Schur forms (Kågström 1993; Kågström & Poromaa 1996 -- the method of
+ * LAPACK xTGEX2) with the readings G1-G6 of DESIGN.md §3:
+ *   G1  1x1|1x1: a Givens pair from the eigenvector of the lower eigenvalue
+ *       (right) and its image under S or T, whichever is relatively larger
+ *       (left).
+ *   G2  other cases: the generalized Sylvester equation
+ *         S11 R - L S22 = S12,  T11 R - L T22 = T12   (scale 1)
+ *       by Gaussian elimination with complete pivoting on its Kronecker
+ *       form (order 2 n1 n2); orthogonal bases of span[-R; I] (right) and
+ *       span[-L; I] (left) by Householder QR.
+ *   G3  weak stability test: the n1 x n2 block below the new leading block
+ *       of each of S and T is at most max(20 eps max|block|, smlnum) of
+ *       that matrix, else the swap is rejected (nothing is changed); passed
+ *       blocks are set to exact zeros.
+ *   G4  standard form: every 2x2 diagonal block of T is diagonal with
+ *       t11 >= t22 > 0 (a 2x2 SVD applied to both matrices); the paired
+ *       2x2 block of S is left general; a moved 1x1 block has t >= 0.  A moved 2x2 block whose pencil has
+ *       real eigenvalues, or a singular 2x2 block of T, rejects the swap.
+ *   G5  accumulators: the left factor U (Q-side) and the right factor V
+ *       (Z-side) of each swap; a window accumulates UL and VR from I.
+ *   G6  updates of a window [j1, j2): (S, T)[j1:j2, j2:n] <- UL^T (.),
+ *       (S, T)[0:j1, j1:j2] <- (.) VR, Q[:, j1:j2] <- Q UL, Z[:, j1:j2] <- Z VR.
+ * ========================================================================= */
+
+/* m x m matrices (m <= 4) column-major with ld 4 */
+static void sm_eye(double* U, int m) {
+  memset(U, 0, 16 * sizeof(double));
+  for (int i = 0; i < m; ++i) U[i + 4 * i] = 1.0;
+}
+
+/* C = A^T B V (all m x m) */
+static void sm_congruence(const double* U, const double* B, const double* V, double* C, int m) {
+  double W[16];
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < m; ++r) {
+      double acc = 0.0;
+      for (int l = 0; l < m; ++l) acc += B[r + 4 * l] * V[l + 4 * c];
+      W[r + 4 * c] = acc;
+    }
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < m; ++r) {
+      double acc = 0.0;
+      for (int l = 0; l < m; ++l) acc += U[l + 4 * r] * W[l + 4 * c];
+      C[r + 4 * c] = acc;
+    }
+}
+
+/* A <- A P (m x m) */
+static void sm_mul_right(double* A, const double* P, int m) {
+  double W[16];
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < m; ++r) {
+      double acc = 0.0;
+      for (int l = 0; l < m; ++l) acc += A[r + 4 * l] * P[l + 4 * c];
+      W[r + 4 * c] = acc;
+    }
+  memcpy(A, W, sizeof(W));
+}
+
+/* rows r0..r0+m-1, columns c0..c1-1 of A <- U^T (those rows) */
+static void apply_left_small(double* A, int64_t lda, int64_t r0, int m, int64_t c0, int64_t c1,
+                             const double* U) {
+  double x[4], y[4];
+  for (int64_t c = c0; c < c1; ++c) {
+    for (int i = 0; i < m; ++i) x[i] = IDX(A, lda, r0 + i, c);
+    for (int i = 0; i < m; ++i) {
+      double acc = 0.0;
+      for (int l = 0; l < m; ++l) acc += U[l + 4 * i] * x[l];
+      y[i] = acc;
+    }
+    for (int i = 0; i < m; ++i) IDX(A, lda, r0 + i, c) = y[i];
+  }
+}
+
+/* columns c0..c0+m-1, rows r0..r1-1 of A <- (those columns) V */
+static void apply_right_small(double* A, int64_t lda, int64_t c0, int m, int64_t r0, int64_t r1,
+                              const double* V) {
+  double x[4], y[4];
+  for (int64_t r = r0; r < r1; ++r) {
+    for (int i = 0; i < m; ++i) x[i] = IDX(A, lda, r, c0 + i);
+    for (int i = 0; i < m; ++i) {
+      double acc = 0.0;
+      for (int l = 0; l < m; ++l) acc += x[l] * V[l + 4 * i];
+      y[i] = acc;
+    }
+    for (int i = 0; i < m; ++i) IDX(A, lda, r, c0 + i) = y[i];
+  }
+}
+
+/* Householder QR of the m x p matrix M (ld 4): H = H_1 ... H_p explicitly (m x m),
+ * H_c = I - 2 v v^T / (v^T v); the first p columns of H span range(M). */
+static void sm_qr_basis(double* M, int m, int p, double* H) {
+  sm_eye(H, m);
+  for (int c = 0; c < p; ++c) {
+    double nrm = 0.0;
+    for (int i = c; i < m; ++i) nrm += M[i + 4 * c] * M[i + 4 * c];
+    nrm = sqrt(nrm);
+    if (nrm == 0.0) continue;
+    double v[4] = {0, 0, 0, 0}, vtv = 0.0;
+    for (int i = c; i < m; ++i) v[i] = M[i + 4 * c];
+    v[c] += copysign(nrm, M[c + 4 * c]);
+    for (int i = c; i < m; ++i) vtv += v[i] * v[i];
+    for (int cc = c; cc < p; ++cc) {
+      double s = 0.0;
+      for (int i = c; i < m; ++i) s += v[i] * M[i + 4 * cc];
+      const double f = 2.0 * s / vtv;
+      for (int i = c; i < m; ++i) M[i + 4 * cc] -= f * v[i];
+    }
+    for (int r = 0; r < m; ++r) {
+      double s = 0.0;
+      for (int i = c; i < m; ++i) s += H[r + 4 * i] * v[i];
+      const double f = 2.0 * s / vtv;
+      for (int i = c; i < m; ++i) H[r + 4 * i] -= f * v[i];
+    }
+  }
+}
+
+int or_gsylv(int n1, int n2, const double* A11, const double* A22, const double* A12,
+             const double* B11, const double* B22, const double* B12, double* R, double* L) {
+  /* unknowns x = [vec R; vec L] (column-major vec, R(i,j) at i + n1*j) */
+  const int N = n1 * n2, K = 2 * N;
+  double M[8][8], rhs[8];
+  memset(M, 0, sizeof(M));
+  for (int jj = 0; jj < n2; ++jj)
+    for (int i = 0; i < n1; ++i) {
+      const int e = i + n1 * jj;
+      /* (A11 R)(i,jj) = sum_l A11(i,l) R(l,jj);  (L A22)(i,jj) = sum_l L(i,l) A22(l,jj) */
+      for (int l = 0; l < n1; ++l) {
+        M[e][l + n1 * jj] += A11[i + 2 * l];
+        M[N + e][l + n1 * jj] += B11[i + 2 * l];
+      }
+      for (int l = 0; l < n2; ++l) {
+        M[e][N + i + n1 * l] -= A22[l + 2 * jj];
+        M[N + e][N + i + n1 * l] -= B22[l + 2 * jj];
+      }
+      rhs[e] = A12[i + 2 * jj];
+      rhs[N + e] = B12[i + 2 * jj];
+    }
+  /* Gaussian elimination with complete pivoting */
+  int perm_c[8], perturbed = 0;
+  for (int q = 0; q < K; ++q) perm_c[q] = q;
+  double mx = 0.0;
+  for (int r = 0; r < K; ++r)
+    for (int c = 0; c < K; ++c) mx = dmax(mx, fabs(M[r][c]));
+  const double smin = dmax(DBL_EPSILON * mx, DBL_MIN / DBL_EPSILON);
+  for (int p = 0; p < K; ++p) {
+    int pr = p, pc = p;
+    double best = -1.0;
+    for (int r = p; r < K; ++r)
+      for (int c = p; c < K; ++c)
+        if (fabs(M[r][c]) > best) { best = fabs(M[r][c]); pr = r; pc = c; }
+    if (pr != p) {
+      for (int c = 0; c < K; ++c) { double t = M[p][c]; M[p][c] = M[pr][c]; M[pr][c] = t; }
+      double t = rhs[p]; rhs[p] = rhs[pr]; rhs[pr] = t;
+    }
+    if (pc != p) {
+      for (int r = 0; r < K; ++r) { double t = M[r][p]; M[r][p] = M[r][pc]; M[r][pc] = t; }
+      int t = perm_c[p]; perm_c[p] = perm_c[pc]; perm_c[pc] = t;
+    }
+    if (fabs(M[p][p]) < smin) { M[p][p] = smin; perturbed = 1; }
+    for (int r = p + 1; r < K; ++r) {
+      const double f = M[r][p] / M[p][p];
+      for (int c = p; c < K; ++c) M[r][c] -= f * M[p][c];
+      rhs[r] -= f * rhs[p];
+    }
+  }
+  double y[8], x[8];
+  for (int p = K - 1; p >= 0; --p) {
+    double acc = rhs[p];
+    for (int c = p + 1; c < K; ++c) acc -= M[p][c] * y[c];
+    y[p] = acc / M[p][p];
+  }
+  for (int p = 0; p < K; ++p) x[perm_c[p]] = y[p];
+  for (int jj = 0; jj < n2; ++jj)
+    for (int i = 0; i < n1; ++i) {
+      R[i + 2 * jj] = x[i + n1 * jj];
+      L[i + 2 * jj] = x[N + i + n1 * jj];
+    }
+  return perturbed;
+}
+
+/* 2x2 standard form of a T block (G4): orthogonal P, W with P^T Tb W = diag(s1, s2),
+ * s1 >= s2 > 0 (one-sided Jacobi on the columns of Tb).  Tb, P, W ld 2.  Returns 1 if Tb
+ * is singular. */
+static int std_t22(const double* Tb, double* P, double* W) {
+  const double a = Tb[0] * Tb[0] + Tb[1] * Tb[1];          /* |col0|^2 */
+  const double b = Tb[2] * Tb[2] + Tb[3] * Tb[3];          /* |col1|^2 */
+  const double g = Tb[0] * Tb[2] + Tb[1] * Tb[3];          /* col0 . col1 */
+  double c = 1.0, s = 0.0;
+  if (g != 0.0) {
+    const double zeta = (b - a) / (2.0 * g);
+    const double t = sgn1(zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+    c = 1.0 / sqrt(1.0 + t * t);
+    s = c * t;
+  }
+  /* W = [c s; -s c]: col0' = c col0 - s col1, col1' = s col0 + c col1 (orthogonal) */
+  W[0] = c; W[1] = -s; W[2] = s; W[3] = c;
+  double u0 = c * Tb[0] - s * Tb[2], u1 = c * Tb[1] - s * Tb[3];
+  double w0 = s * Tb[0] + c * Tb[2], w1 = s * Tb[1] + c * Tb[3];
+  if (lapy2(u0, u1) < lapy2(w0, w1)) {
+    /* order the singular values, s1 >= s2: exchange the columns of W */
+    double t;
+    t = W[0]; W[0] = W[2]; W[2] = t;
+    t = W[1]; W[1] = W[3]; W[3] = t;
+    t = u0; u0 = w0; w0 = t;
+    t = u1; u1 = w1; w1 = t;
+  }
+  const double s1 = lapy2(u0, u1);
+  if (s1 == 0.0) return 1;
+  P[0] = u0 / s1; P[1] = u1 / s1;
+  /* second column orthogonal to the first, oriented so that P(:,1) . col1' > 0 */
+  double p2r = -P[1], p2c = P[0];
+  if (p2r * w0 + p2c * w1 < 0.0) { p2r = -p2r; p2c = -p2c; }
+  P[2] = p2r; P[3] = p2c;
+  if (!(p2r * w0 + p2c * w1 > 0.0)) return 1;
+  return 0;
+}
+
+int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t j, int n1, int n2,
+             double* Ql, int64_t ldq, int64_t nq, double* Zr, int64_t ldz, int64_t nz) {
+  const int m = n1 + n2;
+  double A[16], B[16];
+  memset(A, 0, sizeof(A));
+  memset(B, 0, sizeof(B));
+  double anorm = 0.0, bnorm = 0.0;
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < m; ++r) {
+      A[r + 4 * c] = IDX(S, lds, j + r, j + c);
+      B[r + 4 * c] = IDX(T, ldt, j + r, j + c);
+      anorm = dmax(anorm, fabs(A[r + 4 * c]));
+      bnorm = dmax(bnorm, fabs(B[r + 4 * c]));
+    }
+  const double smlnum = DBL_MIN / DBL_EPSILON;
+  const double threshA = dmax(20.0 * DBL_EPSILON * anorm, smlnum);
+  const double threshB = dmax(20.0 * DBL_EPSILON * bnorm, smlnum);
+  double U[16], V[16];
+  sm_eye(U, m);
+  sm_eye(V, m);
+  if (n1 == 1 && n2 == 1) {
+    /* G1: x spans the null space of b22 A - a22 B = [m11 m12; 0 0] */
+    const double a11 = A[0], a12 = A[4], a22 = A[5], b11 = B[0], b12 = B[4], b22 = B[5];
+    const double m11 = b22 * a11 - a22 * b11, m12 = b22 * a12 - a22 * b12;
+    double c, s, r;
+    or_lartg(m12, -m11, &c, &s, &r);
+    V[0] = c; V[1] = s; V[4] = -s; V[5] = c;               /* V e1 = (c, s) ~ x */
+    const double ax0 = a11 * c + a12 * s, ax1 = a22 * s;
+    const double bx0 = b11 * c + b12 * s, bx1 = b22 * s;
+    const double ra = anorm > 0.0 ? lapy2(ax0, ax1) / anorm : 0.0;
+    const double rb = bnorm > 0.0 ? lapy2(bx0, bx1) / bnorm : 0.0;
+    double c2, s2, r2;
+    if (ra >= rb) or_lartg(ax0, ax1, &c2, &s2, &r2);
+    else or_lartg(bx0, bx1, &c2, &s2, &r2);
+    U[0] = c2; U[1] = s2; U[4] = -s2; U[5] = c2;
+  } else {
+    /* G2 */
+    double A11[4] = {0}, A22[4] = {0}, A12[4] = {0}, B11[4] = {0}, B22[4] = {0}, B12[4] = {0};
+    double R[4] = {0}, L[4] = {0};
+    for (int c = 0; c < n1; ++c)
+      for (int r = 0; r < n1; ++r) { A11[r + 2 * c] = A[r + 4 * c]; B11[r + 2 * c] = B[r + 4 * c]; }
+    for (int c = 0; c < n2; ++c)
+      for (int r = 0; r < n2; ++r) {
+        A22[r + 2 * c] = A[(n1 + r) + 4 * (n1 + c)];
+        B22[r + 2 * c] = B[(n1 + r) + 4 * (n1 + c)];
+      }
+    for (int c = 0; c < n2; ++c)
+      for (int r = 0; r < n1; ++r) { A12[r + 2 * c] = A[r + 4 * (n1 + c)]; B12[r + 2 * c] = B[r + 4 * (n1 + c)]; }
+    or_gsylv(n1, n2, A11, A22, A12, B11, B22, B12, R, L);
+    double Mr[16], Ml[16];
+    memset(Mr, 0, sizeof(Mr));
+    memset(Ml, 0, sizeof(Ml));
+    for (int c = 0; c < n2; ++c) {
+      for (int r = 0; r < n1; ++r) { Mr[r + 4 * c] = -R[r + 2 * c]; Ml[r + 4 * c] = -L[r + 2 * c]; }
+      Mr[(n1 + c) + 4 * c] = 1.0;
+      Ml[(n1 + c) + 4 * c] = 1.0;
+    }
+    sm_qr_basis(Mr, m, n2, V);
+    sm_qr_basis(Ml, m, n2, U);
+  }
+  /* trial */
+  double An[16], Bn[16];
+  sm_congruence(U, A, V, An, m);
+  sm_congruence(U, B, V, Bn, m);
+  /* G3: the block below the new leading n2 x n2 block */
+  double resA = 0.0, resB = 0.0;
+  for (int c = 0; c < n2; ++c)
+    for (int r = n2; r < m; ++r) {
+      resA = dmax(resA, fabs(An[r + 4 * c]));
+      resB = dmax(resB, fabs(Bn[r + 4 * c]));
+    }
+  if (!(resA <= threshA && resB <= threshB)) return 1;
+  for (int c = 0; c < n2; ++c)
+    for (int r = n2; r < m; ++r) { An[r + 4 * c] = 0.0; Bn[r + 4 * c] = 0.0; }
+  /* G4: standard form of each new 2x2 block */
+  int pos[2], np = 0;
+  if (n2 == 2) pos[np++] = 0;
+  if (n1 == 2) pos[np++] = n2;
+  for (int q = 0; q < np; ++q) {
+    const int p = pos[q];
+    double Tb[4] = {Bn[p + 4 * p], Bn[(p + 1) + 4 * p], Bn[p + 4 * (p + 1)], Bn[(p + 1) + 4 * (p + 1)]};
+    double P2[4], W2[4];
+    if (std_t22(Tb, P2, W2)) return 1;
+    double Pm[16], Wm[16];
+    sm_eye(Pm, m);
+    sm_eye(Wm, m);
+    Pm[p + 4 * p] = P2[0]; Pm[(p + 1) + 4 * p] = P2[1]; Pm[p + 4 * (p + 1)] = P2[2]; Pm[(p + 1) + 4 * (p + 1)] = P2[3];
+    Wm[p + 4 * p] = W2[0]; Wm[(p + 1) + 4 * p] = W2[1]; Wm[p + 4 * (p + 1)] = W2[2]; Wm[(p + 1) + 4 * (p + 1)] = W2[3];
+    double A2[16], B2[16];
+    sm_congruence(Pm, An, Wm, A2, m);
+    sm_congruence(Pm, Bn, Wm, B2, m);
+    memcpy(An, A2, sizeof(A2));
+    memcpy(Bn, B2, sizeof(B2));
+    Bn[(p + 1) + 4 * p] = 0.0;
+    Bn[p + 4 * (p + 1)] = 0.0;
+    sm_mul_right(U, Pm, m);
+    sm_mul_right(V, Wm, m);
+    /* complex pair?  eigenvalues of diag(1/t11, 1/t22) * S block */
+    const double t11 = Bn[p + 4 * p], t22 = Bn[(p + 1) + 4 * (p + 1)];
+    const double e11 = An[p + 4 * p] / t11, e12 = An[p + 4 * (p + 1)] / t11;
+    const double e21 = An[(p + 1) + 4 * p] / t22, e22 = An[(p + 1) + 4 * (p + 1)] / t22;
+    const double h = 0.5 * (e11 - e22);
+    if (!(h * h + e12 * e21 < 0.0)) return 1;
+  }
+  /* G4: a new 1x1 block has t >= 0 (negate its row of the pencil and its column of U) */
+  int one[2], no = 0;
+  if (n2 == 1) one[no++] = 0;
+  if (n1 == 1) one[no++] = n2;
+  for (int q = 0; q < no; ++q) {
+    const int p = one[q];
+    if (Bn[p + 4 * p] < 0.0) {
+      for (int c = 0; c < m; ++c) { An[p + 4 * c] = -An[p + 4 * c]; Bn[p + 4 * c] = -Bn[p + 4 * c]; }
+      for (int r = 0; r < m; ++r) U[r + 4 * p] = -U[r + 4 * p];
+    }
+  }
+  /* commit */
+  apply_left_small(S, lds, j, m, j + m, nt, U);
+  apply_left_small(T, ldt, j, m, j + m, nt, U);
+  apply_right_small(S, lds, j, m, 0, j, V);
+  apply_right_small(T, ldt, j, m, 0, j, V);
+  if (Ql) apply_right_small(Ql, ldq, j, m, 0, nq, U);
+  if (Zr) apply_right_small(Zr, ldz, j, m, 0, nz, V);
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < m; ++r) {
+      IDX(S, lds, j + r, j + c) = An[r + 4 * c];
+      IDX(T, ldt, j + r, j + c) = Bn[r + 4 * c];
+    }
+  return 0;
+}
+
+/* G6: the updates of one window of the generalized reordering (naive loops) */
+static void gpanel_left(int64_t n, double* A, int64_t lda, int64_t j1, int64_t j2, const double* U,
+                        double* tmp) {
+  const int64_t k = j2 - j1;
+  for (int64_t c = j2; c < n; ++c) {
+    for (int64_t r = 0; r < k; ++r) {
+      double acc = 0.0;
+      for (int64_t l = 0; l < k; ++l) acc += U[l + r * k] * IDX(A, lda, j1 + l, c);
+      tmp[r] = acc;
+    }
+    for (int64_t r = 0; r < k; ++r) IDX(A, lda, j1 + r, c) = tmp[r];
+  }
+}
+
+static void gpanel_right(int64_t rows, double* A, int64_t lda, int64_t j1, int64_t j2, const double* V,
+                         double* tmp) {
+  const int64_t k = j2 - j1;
+  for (int64_t r = 0; r < rows; ++r) {
+    for (int64_t c = 0; c < k; ++c) {
+      double acc = 0.0;
+      for (int64_t l = 0; l < k; ++l) acc += IDX(A, lda, r, j1 + l) * V[l + c * k];
+      tmp[c] = acc;
+    }
+    for (int64_t c = 0; c < k; ++c) IDX(A, lda, r, j1 + c) = tmp[c];
+  }
+}
+
+int or_greorder(int mode, int64_t n, double* S, int64_t lds, double* T, int64_t ldt,
+                double* Q, int64_t ldq, double* Z, int64_t ldz, int32_t* select, int64_t* m,
+                int64_t w, int64_t max_windows, int64_t force_reject_at, int8_t* bmap_out,
+                or_stats* st) {
+  if (mode != 0 && mode != 1) return -1;
+  if (n < 0) return -2;
+  if (n > 0 && (S == NULL || T == NULL)) return -3;
+  if (lds < (n > 1 ? n : 1)) return -4;
+  if (ldt < (n > 1 ? n : 1)) return -6;
+  if (Q && ldq < (n > 1 ? n : 1)) return -8;
+  if (Z && ldz < (n > 1 ? n : 1)) return -10;
+  if (n > 0 && select == NULL) return -11;
+  if (m == NULL) return -12;
+  if (w < 4) return -13;
+  or_stats local;
+  if (!st) st = &local;
+  memset(st, 0, sizeof(*st));
+  st->rejected_window = -1; st->rejected_swap = -1; st->rejected_row = -1;
+  *m = 0;
+  if (n == 0) return 0;
+  /* T upper triangular (exact zeros below the diagonal) */
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t r = c + 1; r < n; ++r)
+      if (IDX(T, ldt, r, c) != 0.0) return -5;
+
+  int8_t* bmap = (int8_t*)malloc((size_t)n);
+  int8_t* selrow = (int8_t*)malloc((size_t)n);
+  if (or_scan(n, S, lds, bmap)) { free(bmap); free(selrow); return -3; }
+  or_select(n, bmap, select, selrow, m);
+
+  sched_t sc;
+  sched_init(&sc, n, bmap, selrow, w);
+  int64_t cap = max_swaps_per_window(w);
+  int64_t* tj = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
+  int8_t* t1 = (int8_t*)malloc((size_t)cap);
+  int8_t* t2 = (int8_t*)malloc((size_t)cap);
+  double* DS = (double*)malloc(sizeof(double) * (size_t)w * (size_t)w);
+  double* DT = (double*)malloc(sizeof(double) * (size_t)w * (size_t)w);
+  double* UL = (double*)malloc(sizeof(double) * (size_t)w * (size_t)w);
+  double* VR = (double*)malloc(sizeof(double) * (size_t)w * (size_t)w);
+  double* tmp = (double*)malloc(sizeof(double) * (size_t)w);
+  int rc = 0;
+  int64_t j1, j2, k, gswap = 0;
+  while ((max_windows < 0 || st->windows < max_windows) &&
+         (k = sched_next(&sc, &j1, &j2, tj, t1, t2)) >= 0) {
+    const int64_t kw = j2 - j1;
+    int64_t done = 0;
+    if (mode == 0) {
+      for (; done < k; ++done) {
+        if (gswap + done == force_reject_at ||
+            or_gswap(n, S, lds, T, ldt, tj[done], t1[done], t2[done], Q, ldq, Q ? n : 0, Z, ldz, Z ? n : 0)) {
+          rc = 1; break;
+        }
+        st->swaps_by_type[(t1[done] - 1) * 2 + (t2[done] - 1)]++;
+      }
+    } else {
+      for (int64_t c = 0; c < kw; ++c)
+        for (int64_t r = 0; r < kw; ++r) {
+          DS[r + c * kw] = IDX(S, lds, j1 + r, j1 + c);
+          DT[r + c * kw] = IDX(T, ldt, j1 + r, j1 + c);
+          UL[r + c * kw] = VR[r + c * kw] = (r == c) ? 1.0 : 0.0;
+        }
+      for (; done < k; ++done) {
+        if (gswap + done == force_reject_at ||
+            or_gswap(kw, DS, kw, DT, kw, tj[done] - j1, t1[done], t2[done], UL, kw, kw, VR, kw, kw)) {
+          rc = 1; break;
+        }
+        st->swaps_by_type[(t1[done] - 1) * 2 + (t2[done] - 1)]++;
+      }
+      for (int64_t c = 0; c < kw; ++c)
+        for (int64_t r = 0; r < kw; ++r) {
+          IDX(S, lds, j1 + r, j1 + c) = DS[r + c * kw];
+          IDX(T, ldt, j1 + r, j1 + c) = DT[r + c * kw];
+        }
+      gpanel_left(n, S, lds, j1, j2, UL, tmp);
+      gpanel_left(n, T, ldt, j1, j2, UL, tmp);
+      gpanel_right(j1, S, lds, j1, j2, VR, tmp);
+      gpanel_right(j1, T, ldt, j1, j2, VR, tmp);
+      if (Q) gpanel_right(n, Q, ldq, j1, j2, UL, tmp);
+      if (Z) gpanel_right(n, Z, ldz, j1, j2, VR, tmp);
+    }
+    st->swaps += done;
+    st->windows++;
+    st->eq_flops += 2.0 * kw * kw * (2.0 * (double)(n - j2) + 2.0 * (double)j1 + (Q ? (double)n : 0.0) +
+                                     (Z ? (double)n : 0.0));
+    if (rc) {
+      st->rejected_window = st->windows - 1;
+      st->rejected_swap = gswap + done;
+      st->rejected_row = tj[done];
+      st->rejected_n1 = t1[done];
+      st->rejected_n2 = t2[done];
+      sched_rollback(&sc, tj, k, done);
+      break;
+    }
+    gswap += k;
+  }
+  for (int64_t b = 0; b < sc.B; ++b) {
+    int64_t r = sc.brow[b];
+    for (int q = 0; q < sc.bsz[b]; ++q) {
+      select[r + q] = sc.bsel[b];
+      if (bmap_out) bmap_out[r + q] = (int8_t)(sc.bsz[b] == 1 ? 0 : 1 + q);
+    }
+  }
+  free(tj); free(t1); free(t2); free(DS); free(DT); free(UL); free(VR); free(tmp);
   free(bmap); free(selrow);
   sched_free(&sc);
   return rc;

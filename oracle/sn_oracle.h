@@ -115,6 +115,35 @@ int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t l
                int32_t* select, int64_t* m, int64_t w, int64_t max_windows,
                int64_t force_reject_at, int8_t* bmap_out, or_stats* st);
 
+/* ---- generalized reordering (Eq. (7) right form; Table 1
+ * P:216).  Readings G1-G6 in sn_oracle.c and DESIGN.md §3. ----
+ *
+ * Generalized Sylvester pair (G2): S11 R - L S22 = S12, T11 R - L T22 = T12 for
+ * n1, n2 in {1, 2} (all blocks column-major with ld 2), by Gaussian elimination
+ * with complete pivoting on the Kronecker system of order 2 n1 n2.  Returns 1 if a
+ * pivot was perturbed (near-common eigenvalue), else 0. */
+int or_gsylv(int n1, int n2, const double* A11, const double* A22, const double* A12,
+             const double* B11, const double* B22, const double* B12, double* R, double* L);
+
+/* Swap the adjacent diagonal blocks of sizes n1 (row j) and n2 (row j+n1) of the
+ * nt x nt pencil (S, T) in generalized real Schur form (S quasi-triangular, T upper
+ * triangular with diagonal 2x2 blocks).  (S, T) <- U^T (S, T) V on rows/columns
+ * j..j+n1+n2-1 (rows right of the block, columns above it, the block itself);
+ * Ql (nq rows, may be NULL) <- Ql U and Zr (nz rows, may be NULL) <- Zr V on the same
+ * columns.  Returns 0, or 1 if the swap is rejected (G3/G4; nothing modified). */
+int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t j, int n1, int n2,
+             double* Ql, int64_t ldq, int64_t nq, double* Zr, int64_t ldz, int64_t nz);
+
+/* Generalized reordering (S, T) = Q3 (Ŝ, T̂) Z3^T, Q <- Q Q3, Z <- Z Z3 (Q, Z may be
+ * NULL), with the schedule of or_reorder (it depends only on the block map of S and
+ * the selection).  mode 0 = swaps applied to the full matrices, 1 = per window
+ * accumulated UL/VR and naive panel updates (G6).  Other arguments and the return
+ * value as or_reorder; -5 if T has a nonzero below its diagonal. */
+int or_greorder(int mode, int64_t n, double* S, int64_t lds, double* T, int64_t ldt,
+                double* Q, int64_t ldq, double* Z, int64_t ldz, int32_t* select, int64_t* m,
+                int64_t w, int64_t max_windows, int64_t force_reject_at, int8_t* bmap_out,
+                or_stats* st);
+
 #ifdef __cplusplus
 }
 #endif

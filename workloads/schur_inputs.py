@@ -86,6 +86,7 @@ def normal(seed: int, stream: int, idx: torch.Tensor) -> torch.Tensor:
 
 # streams
 _ST_SHUF, _ST_EIG, _ST_A, _ST_B, _ST_C, _ST_SGN, _ST_UPPER, _ST_Q, _ST_SEL = range(1, 10)
+_ST_TUP, _ST_TDIAG, _ST_Z = range(10, 13)      # pencils (make_pencil)
 
 
 def _uni_np(seed, stream, idx):
@@ -178,7 +179,7 @@ def _schur_form(n, sizes, seed, device, col_block=1024):
     return St, starts
 
 
-def _householder_product_T(n, seed, device, nb=128):
+def _householder_product_T(n, seed, device, nb=128, stream=_ST_Q):
     """Returns X = Q^T (row-major tensor), so X's memory is column-major Q,
     Q = H_0 H_1 ... H_{n-1}, H_i = I - tau_i v_i v_i^T, tau_i = 2 / v_i^T v_i."""
     X = torch.eye(n, dtype=torch.float64, device=device)
@@ -186,7 +187,7 @@ def _householder_product_T(n, seed, device, nb=128):
     for k0 in range(0, n, nb):
         k1 = min(n, k0 + nb)
         ks = torch.arange(k0, k1, device=device, dtype=torch.int64)
-        V = normal(seed, _ST_Q, ks[None, :] * n + rows[:, None])      # (n, nb), column i = v_{k0+i}
+        V = normal(seed, stream, ks[None, :] * n + rows[:, None])     # (n, nb), column i = v_{k0+i}
         G = (V.t() @ V).cpu().numpy()
         m = k1 - k0
         tau = 2.0 / np.diag(G)
@@ -240,3 +241,59 @@ def make_config(cfg: int, seed: int = 1, device="cpu") -> Problem:
     c = CONFIGS[cfg]
     return make_problem(c["n"], c["p2"], c["q"], c["sel"], c["psel"], c["w"], seed=seed, device=device,
                         name="config%d" % cfg)
+
+
+# ---- pencils (generalized reordering) ------------------------------
+
+@dataclasses.dataclass
+class Pencil:
+    n: int
+    S: torch.Tensor            # (n, n) row-major tensor holding S^T (= column-major S)
+    T: torch.Tensor            # same layout, upper triangular
+    Q: torch.Tensor | None
+    Z: torch.Tensor | None
+    select: np.ndarray
+    w: int
+    bsizes: np.ndarray
+    meta: dict
+
+    def np(self, name):
+        x = getattr(self, name)
+        return None if x is None else x.cpu().numpy().T
+
+
+def make_pencil(n: int, p2: float = 0.25, q: str = "householder", sel: str = "bernoulli",
+                psel: float | None = 0.35, w: int = 128, seed: int = 1, device="cpu") -> Pencil:
+    """A generalized real Schur form (S, T) with orthogonal Q, Z (input recipe).
+
+    The paper has no generalized workload; the recipe extends the standard one: S exactly as
+    make_problem; T upper triangular with iid N(0, 1) strictly upper entries, diagonal
+    U[0.5, 2], and at the first row r of every 2x2 block of S: T[r, r+1] = 0 and T[r+1, r+1] =
+    T[r, r] (the 2x2 diagonal block of T is a positive multiple of I, so the block pencil keeps
+    the complex pair of S's standardised block); Q and Z independent Householder products (or
+    I / None)."""
+    base = make_problem(n, p2, q, sel, psel, w, seed, device)
+    device = torch.device(device)
+    sizes = base.bsizes
+    Tt = torch.empty((n, n), dtype=torch.float64, device=device)   # Tt[j, i] = T[i, j]
+    rows = torch.arange(n, device=device, dtype=torch.int64)
+    for c0 in range(0, n, 1024):
+        c1 = min(n, c0 + 1024)
+        cols = torch.arange(c0, c1, device=device, dtype=torch.int64)
+        val = normal(seed, _ST_TUP, cols[:, None] * n + rows[None, :])
+        Tt[c0:c1] = torch.where(rows[None, :] < cols[:, None], val, torch.zeros((), dtype=val.dtype, device=device))
+    Tt[rows, rows] = 0.5 + 1.5 * uniform(seed, _ST_TDIAG, rows)
+    starts = np.concatenate([[0], np.cumsum(sizes.astype(np.int64))[:-1]])
+    r2 = starts[sizes == 2]
+    if len(r2):
+        r = torch.as_tensor(r2, device=device)
+        Tt[r + 1, r] = 0.0                                          # T[r, r+1] = 0
+        Tt[r + 1, r + 1] = Tt[r, r]                                 # T[r+1, r+1] = T[r, r]
+    if q == "identity":
+        Z = torch.eye(n, dtype=torch.float64, device=device)
+    elif q == "householder":
+        Z = _householder_product_T(n, seed, device, stream=_ST_Z)
+    else:
+        Z = None
+    meta = dict(base.meta, kind="pencil")
+    return Pencil(n=n, S=base.S, T=Tt, Q=base.Q, Z=Z, select=base.select, w=w, bsizes=sizes, meta=meta)
