@@ -792,7 +792,10 @@ int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t l
  *         S11 R - L S22 = S12,  T11 R - L T22 = T12   (scale 1)
  *       by Gaussian elimination with complete pivoting on its Kronecker
  *       form (order 2 n1 n2); orthogonal bases of span[-R; I] (right) and
- *       span[-L; I] (left) by Householder QR.
+ *       span[-L; I] (left) by Householder QR.  G2b: if that pair fails the
+ *       weak test (G3), T's block is re-triangularised (as xTGEX2 does) from
+ *       the left or from the right, whichever leaves the smaller S block
+ *       below the new leading block, and the test is applied to that.
  *   G3  weak stability test: the n1 x n2 block below the new leading block
  *       of each of S and T is at most max(20 eps max|block|, smlnum) of
  *       that matrix, else the swap is rejected (nothing is changed); passed
@@ -964,6 +967,14 @@ int or_gsylv(int n1, int n2, const double* A11, const double* A22, const double*
   return perturbed;
 }
 
+/* Frobenius norm of the n1 x n2 block below the leading n2 x n2 block (G3) */
+static double lowblock_fro(const double* X, int n1, int n2) {
+  double acc = 0.0;
+  for (int c = 0; c < n2; ++c)
+    for (int r = n2; r < n1 + n2; ++r) acc += X[r + 4 * c] * X[r + 4 * c];
+  return sqrt(acc);
+}
+
 /* 2x2 standard form of a T block (G4): orthogonal P, W with P^T Tb W = diag(s1, s2),
  * s1 >= s2 > 0 (one-sided Jacobi on the columns of Tb).  Tb, P, W ld 2.  Returns 1 if Tb
  * is singular. */
@@ -1007,14 +1018,16 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
   double A[16], B[16];
   memset(A, 0, sizeof(A));
   memset(B, 0, sizeof(B));
-  double anorm = 0.0, bnorm = 0.0;
+  double anorm = 0.0, bnorm = 0.0;      /* Frobenius norms of the blocks (G3) */
   for (int c = 0; c < m; ++c)
     for (int r = 0; r < m; ++r) {
       A[r + 4 * c] = IDX(S, lds, j + r, j + c);
       B[r + 4 * c] = IDX(T, ldt, j + r, j + c);
-      anorm = dmax(anorm, fabs(A[r + 4 * c]));
-      bnorm = dmax(bnorm, fabs(B[r + 4 * c]));
+      anorm += A[r + 4 * c] * A[r + 4 * c];
+      bnorm += B[r + 4 * c] * B[r + 4 * c];
     }
+  anorm = sqrt(anorm);
+  bnorm = sqrt(bnorm);
   const double smlnum = DBL_MIN / DBL_EPSILON;
   const double threshA = dmax(20.0 * DBL_EPSILON * anorm, smlnum);
   const double threshB = dmax(20.0 * DBL_EPSILON * bnorm, smlnum);
@@ -1065,13 +1078,50 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
   double An[16], Bn[16];
   sm_congruence(U, A, V, An, m);
   sm_congruence(U, B, V, Bn, m);
-  /* G3: the block below the new leading n2 x n2 block */
+  if (!(n1 == 1 && n2 == 1) && !(lowblock_fro(An, n1, n2) <= threshA && lowblock_fro(Bn, n1, n2) <= threshB)) {
+      /* G2b (xTGEX2): make T's block below the new leading block zero to working accuracy,
+       * either from the left (U from a QR of the first n2 columns of T V) or from the right (V
+       * completing the row space of the last n1 rows of U^T T); keep the variant whose S block
+       * below the new leading block is smaller (Frobenius norm). */
+      double Uq[16], Vr[16], TV[16], UT[16], Mq[16], Mrr[16], H[16], I4[16];
+      sm_eye(I4, m);
+      sm_congruence(I4, B, V, TV, m);                 /* T V */
+      sm_congruence(U, B, I4, UT, m);                 /* U^T T */
+      memset(Mq, 0, sizeof(Mq));
+      memset(Mrr, 0, sizeof(Mrr));
+      for (int c = 0; c < n2; ++c)
+        for (int r = 0; r < m; ++r) Mq[r + 4 * c] = TV[r + 4 * c];
+      for (int c = 0; c < n1; ++c)
+        for (int r = 0; r < m; ++r) Mrr[r + 4 * c] = UT[(n2 + c) + 4 * r];
+      sm_qr_basis(Mq, m, n2, Uq);
+      sm_qr_basis(Mrr, m, n1, H);
+      /* V_r: the complement of the row space first, then the row space */
+      memset(Vr, 0, sizeof(Vr));
+      for (int c = 0; c < n2; ++c)
+        for (int r = 0; r < m; ++r) Vr[r + 4 * c] = H[r + 4 * (n1 + c)];
+      for (int c = 0; c < n1; ++c)
+        for (int r = 0; r < m; ++r) Vr[r + 4 * (n2 + c)] = H[r + 4 * c];
+      double Aq[16], Ar[16];
+      sm_congruence(Uq, A, V, Aq, m);
+      sm_congruence(U, A, Vr, Ar, m);
+      double rq = 0.0, rr = 0.0;
+      for (int c = 0; c < n2; ++c)
+        for (int r = n2; r < m; ++r) { rq += Aq[r + 4 * c] * Aq[r + 4 * c]; rr += Ar[r + 4 * c] * Ar[r + 4 * c]; }
+      if (rq <= rr) memcpy(U, Uq, sizeof(Uq));
+      else memcpy(V, Vr, sizeof(Vr));
+
+    sm_congruence(U, A, V, An, m);
+    sm_congruence(U, B, V, Bn, m);
+  }
+  /* G3: Frobenius norm of the block below the new leading n2 x n2 block */
   double resA = 0.0, resB = 0.0;
   for (int c = 0; c < n2; ++c)
     for (int r = n2; r < m; ++r) {
-      resA = dmax(resA, fabs(An[r + 4 * c]));
-      resB = dmax(resB, fabs(Bn[r + 4 * c]));
+      resA += An[r + 4 * c] * An[r + 4 * c];
+      resB += Bn[r + 4 * c] * Bn[r + 4 * c];
     }
+  resA = sqrt(resA);
+  resB = sqrt(resB);
   if (!(resA <= threshA && resB <= threshB)) return 1;
   for (int c = 0; c < n2; ++c)
     for (int r = n2; r < m; ++r) { An[r + 4 * c] = 0.0; Bn[r + 4 * c] = 0.0; }
