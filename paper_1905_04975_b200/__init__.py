@@ -75,7 +75,7 @@ SN_OK, SN_ERR_REJECTED, SN_ERR_CUDA, SN_ERR_NCCL, SN_ERR_UNSUPPORTED = 0, 1, 2, 
 EXPORTS = ["sn_default_opts", "sn_strerror", "sn_reorder_schur", "sn_reorder_schur_ex",
            "sn_schedule_build", "sn_schedule_lookahead", "sn_schedule_window_swaps", "sn_version",
            "sn_dist_unique_id", "sn_dist_init", "sn_dist_finalize", "sn_dist_layout", "sn_reorder_schur_dist",
-           "sn_reorder_schur_dist_local", "sn_dist_program", "sn_release_workspace"]
+           "sn_reorder_schur_dist_local", "sn_dist_program", "sn_release_workspace", "sn_reorder_pencil_ex"]
 
 _lib = None
 
@@ -120,6 +120,9 @@ def lib():
         L.sn_reorder_schur_dist_local.restype = C.c_int
         L.sn_dist_program.argtypes = [i64, p, p, i64, i64, i64, i64, i64, p]
         L.sn_dist_program.restype = i64
+        L.sn_reorder_pencil_ex.argtypes = [C.POINTER(Opts), i64, p, i64, p, i64, p, i64, p, i64, p, C.POINTER(i64),
+                                           p, C.POINTER(Stats), p]
+        L.sn_reorder_pencil_ex.restype = C.c_int
         _lib = L
     return _lib
 
@@ -178,6 +181,29 @@ def reorder(S, Q, select, window: int = 256, stream=None, **opts):
     rc = lib().sn_reorder_schur_ex(C.byref(o), n, ps, n, pq, n, sel.ctypes.data_as(C.c_void_p), C.byref(m),
                                    bmap.ctypes.data_as(C.c_void_p), C.byref(st),
                                    None if stream is None else C.c_void_p(stream))
+    return {"rc": rc, "m": m.value, "select": sel, "bmap": bmap, "stats": st.to_dict()}
+
+
+def reorder_pencil(S, T, Q, Z, select, window: int = 256, stream=None, **opts):
+    """Generalized reordering in place (sn_reorder_pencil_ex).  S, T, Q, Z: CUDA torch fp64
+    tensors (column-major memory, see module doc); Q and/or Z may be None.  Returns dict(rc, m,
+    select, bmap, stats)."""
+    import torch
+    ps, n = _tensor_ptr(S)
+    pt, nt = _tensor_ptr(T)
+    pq, nq = _tensor_ptr(Q)
+    pz, nz = _tensor_ptr(Z)
+    assert nt == n and (Q is None or nq == n) and (Z is None or nz == n)
+    o = default_opts(window=window, **opts)
+    sel = np.ascontiguousarray(select, np.int32).copy()
+    bmap = np.zeros(n, np.int8)
+    m = C.c_int64()
+    st = Stats()
+    if stream is None and S.is_cuda:
+        stream = torch.cuda.current_stream(S.device).cuda_stream
+    rc = lib().sn_reorder_pencil_ex(C.byref(o), n, ps, n, pt, n, pq, n, pz, n, sel.ctypes.data_as(C.c_void_p),
+                                    C.byref(m), bmap.ctypes.data_as(C.c_void_p), C.byref(st),
+                                    None if stream is None else C.c_void_p(stream))
     return {"rc": rc, "m": m.value, "select": sel, "bmap": bmap, "stats": st.to_dict()}
 
 

@@ -1,0 +1,754 @@
+// sn_pencil.cu -- generalized reordering of a matrix pencil (PAPER.md
+// Eq. (7) right form: (S, T) = Q3 (Ŝ, T̂) Z3^T; Table 1).  Product code.
+//
+// Same schedule, levels and panel kernels as the standard path (sn_plan.cpp,
+// sn_kernels_panel*.cu); what differs is the window task and that every window carries two
+// accumulators: UL (left factors, applied as UL^T to the rows right of the window of S and
+// T, and to the columns of Q) and VR (right factors, applied to the columns above the window
+// of S and T, and to the columns of Z).  The swap transform is the direct swap of generalized
+// real Schur forms with the readings G1-G6 of DESIGN.md §3.1 (1x1|1x1: a Givens pair from the
+// eigenvector of the lower eigenvalue; otherwise the generalized Sylvester pair by complete
+// pivoting on its Kronecker form, bases of span[-R; I] and span[-L; I] by Householder QR; the
+// weak stability test; T's 2x2 blocks diagonal with t11 >= t22 > 0 by a 2x2 SVD; moved 1x1
+// blocks with t >= 0).
+//
+// First version (correctness first): one CTA per window, one thread evaluates each swap's
+// transform, 256 threads apply it to the window of S and T (in place in global memory, L2
+// resident) and to UL / VR; the column nonzero intervals of the accumulators are tracked as
+// in the standard window kernel so the panel kernels skip structural zeros.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "sn_device.cuh"
+#include "sn_exec.h"
+#include "sn_plan.h"
+#include "sn_reorder.h"
+
+namespace sn {
+namespace {
+
+// ---------------------------------------------------------------- the swap transform (device)
+// 4x4 matrices column-major with ld 4 in per-thread arrays.
+
+__host__ __device__ void pl_lartg(double f, double g, double& c, double& s, double& r) {
+  // c >= 0, r = sign(f) hypot(f, g), [c s; -s c] [f; g] = [r; 0]
+  if (g == 0.0) { c = 1.0; s = 0.0; r = f; return; }
+  if (f == 0.0) { c = 0.0; s = copysign(1.0, g); r = fabs(g); return; }
+  const double d = hypot(f, g);
+  c = fabs(f) / d;
+  r = copysign(d, f);
+  s = g / r;
+}
+
+__host__ __device__ void pl_eye(double* U, int m) {
+  for (int i = 0; i < 16; ++i) U[i] = 0.0;
+  for (int i = 0; i < m; ++i) U[i * 5] = 1.0;
+}
+
+// C = U^T X V
+__host__ __device__ void pl_congr(const double* U, const double* X, const double* V, double* C, int m) {
+  double W[16];
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < m; ++r) {
+      double acc = 0.0;
+      for (int l = 0; l < m; ++l) acc = fma(X[r + 4 * l], V[l + 4 * c], acc);
+      W[r + 4 * c] = acc;
+    }
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < m; ++r) {
+      double acc = 0.0;
+      for (int l = 0; l < m; ++l) acc = fma(U[l + 4 * r], W[l + 4 * c], acc);
+      C[r + 4 * c] = acc;
+    }
+}
+
+// X <- X P
+__host__ __device__ void pl_mulr(double* X, const double* P, int m) {
+  double W[16];
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < m; ++r) {
+      double acc = 0.0;
+      for (int l = 0; l < m; ++l) acc = fma(X[r + 4 * l], P[l + 4 * c], acc);
+      W[r + 4 * c] = acc;
+    }
+  for (int i = 0; i < 16; ++i) X[i] = W[i];
+}
+
+// orthogonal H (m x m) whose first p columns span range(M) (M: m x p, destroyed)
+__host__ __device__ void pl_qr_basis(double* M, int m, int p, double* H) {
+  pl_eye(H, m);
+  for (int c = 0; c < p; ++c) {
+    double nrm = 0.0;
+    for (int i = c; i < m; ++i) nrm = fma(M[i + 4 * c], M[i + 4 * c], nrm);
+    nrm = sqrt(nrm);
+    if (nrm == 0.0) continue;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = c; i < m; ++i) v[i] = M[i + 4 * c];
+    v[c] += copysign(nrm, M[c + 4 * c]);
+    double vtv = 0.0;
+    for (int i = c; i < m; ++i) vtv = fma(v[i], v[i], vtv);
+    const double f2 = 2.0 / vtv;
+    for (int cc = c; cc < p; ++cc) {
+      double s = 0.0;
+      for (int i = c; i < m; ++i) s = fma(v[i], M[i + 4 * cc], s);
+      for (int i = c; i < m; ++i) M[i + 4 * cc] -= (f2 * s) * v[i];
+    }
+    for (int r = 0; r < m; ++r) {
+      double s = 0.0;
+      for (int i = c; i < m; ++i) s = fma(H[r + 4 * i], v[i], s);
+      for (int i = c; i < m; ++i) H[r + 4 * i] -= (f2 * s) * v[i];
+    }
+  }
+}
+
+// Generalized Sylvester pair S11 R - L S22 = S12, T11 R - L T22 = T12 (G2): Kronecker system
+// x = [vec R; vec L] (column-major vec) by Gaussian elimination with complete pivoting.
+// A = the m x m block of S, B = of T (ld 4).  R, L: n1 x n2 with ld 2.
+__host__ __device__ void pl_gsylv(const double* A, const double* B, int n1, int n2, double* R, double* L) {
+  const int N = n1 * n2, K = 2 * N;
+  double M[8][8], y[8];
+  int cp[8];
+  for (int r = 0; r < 8; ++r)
+    for (int c = 0; c < 8; ++c) M[r][c] = 0.0;
+  for (int jj = 0; jj < n2; ++jj)
+    for (int i = 0; i < n1; ++i) {
+      const int e = i + n1 * jj;
+      for (int l = 0; l < n1; ++l) {
+        M[e][l + n1 * jj] += A[i + 4 * l];
+        M[N + e][l + n1 * jj] += B[i + 4 * l];
+      }
+      for (int l = 0; l < n2; ++l) {
+        M[e][N + i + n1 * l] -= A[(n1 + l) + 4 * (n1 + jj)];
+        M[N + e][N + i + n1 * l] -= B[(n1 + l) + 4 * (n1 + jj)];
+      }
+      y[e] = A[i + 4 * (n1 + jj)];
+      y[N + e] = B[i + 4 * (n1 + jj)];
+    }
+  double mx = 0.0;
+  for (int r = 0; r < K; ++r)
+    for (int c = 0; c < K; ++c) mx = fmax(mx, fabs(M[r][c]));
+  const double smin = fmax(2.220446049250313e-16 * mx, 2.2250738585072014e-308 / 2.220446049250313e-16);
+  for (int q = 0; q < K; ++q) cp[q] = q;
+  for (int p = 0; p < K; ++p) {
+    int pr = p, pc = p;
+    double best = -1.0;
+    for (int r = p; r < K; ++r)
+      for (int c = p; c < K; ++c)
+        if (fabs(M[r][c]) > best) { best = fabs(M[r][c]); pr = r; pc = c; }
+    if (pr != p) {
+      for (int c = 0; c < K; ++c) { const double t = M[p][c]; M[p][c] = M[pr][c]; M[pr][c] = t; }
+      const double t = y[p]; y[p] = y[pr]; y[pr] = t;
+    }
+    if (pc != p) {
+      for (int r = 0; r < K; ++r) { const double t = M[r][p]; M[r][p] = M[r][pc]; M[r][pc] = t; }
+      const int t = cp[p]; cp[p] = cp[pc]; cp[pc] = t;
+    }
+    if (fabs(M[p][p]) < smin) M[p][p] = smin;
+    const double ip = 1.0 / M[p][p];
+    for (int r = p + 1; r < K; ++r) {
+      const double f = M[r][p] * ip;
+      for (int c = p; c < K; ++c) M[r][c] -= f * M[p][c];
+      y[r] -= f * y[p];
+    }
+  }
+  double x[8], z[8];
+  for (int p = K - 1; p >= 0; --p) {
+    double acc = y[p];
+    for (int c = p + 1; c < K; ++c) acc -= M[p][c] * z[c];
+    z[p] = acc / M[p][p];
+  }
+  for (int p = 0; p < K; ++p) x[cp[p]] = z[p];
+  for (int jj = 0; jj < n2; ++jj)
+    for (int i = 0; i < n1; ++i) {
+      R[i + 2 * jj] = x[i + n1 * jj];
+      L[i + 2 * jj] = x[N + i + n1 * jj];
+    }
+}
+
+// Frobenius norm of the n1 x n2 block below the leading n2 x n2 block (G3)
+__host__ __device__ double pl_lowfro(const double* X, int n1, int n2) {
+  double acc = 0.0;
+  for (int c = 0; c < n2; ++c)
+    for (int r = n2; r < n1 + n2; ++r) acc = fma(X[r + 4 * c], X[r + 4 * c], acc);
+  return sqrt(acc);
+}
+
+// 2x2 SVD of a T block (G4): P^T Tb W = diag(s1, s2), s1 >= s2 > 0.  Tb, P, W ld 2.
+// Returns false if Tb is singular.
+__host__ __device__ bool pl_std_t22(const double* Tb, double* P, double* W) {
+  const double a = Tb[0] * Tb[0] + Tb[1] * Tb[1];
+  const double b = Tb[2] * Tb[2] + Tb[3] * Tb[3];
+  const double g = Tb[0] * Tb[2] + Tb[1] * Tb[3];
+  double c = 1.0, s = 0.0;
+  if (g != 0.0) {
+    const double zeta = (b - a) / (2.0 * g);
+    const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+    c = 1.0 / sqrt(1.0 + t * t);
+    s = c * t;
+  }
+  W[0] = c; W[1] = -s; W[2] = s; W[3] = c;
+  double u0 = c * Tb[0] - s * Tb[2], u1 = c * Tb[1] - s * Tb[3];
+  double w0 = s * Tb[0] + c * Tb[2], w1 = s * Tb[1] + c * Tb[3];
+  if (hypot(u0, u1) < hypot(w0, w1)) {
+    double t;
+    t = W[0]; W[0] = W[2]; W[2] = t;
+    t = W[1]; W[1] = W[3]; W[3] = t;
+    t = u0; u0 = w0; w0 = t;
+    t = u1; u1 = w1; w1 = t;
+  }
+  const double s1 = hypot(u0, u1);
+  if (s1 == 0.0) return false;
+  P[0] = u0 / s1; P[1] = u1 / s1;
+  double p2r = -P[1], p2c = P[0];
+  if (p2r * w0 + p2c * w1 < 0.0) { p2r = -p2r; p2c = -p2c; }
+  P[2] = p2r; P[3] = p2c;
+  return p2r * w0 + p2c * w1 > 0.0;
+}
+
+// The transform of one swap (G1-G4).  A, B: the m x m blocks of S and T (ld 4, m = n1 + n2).
+// Out: U, V (m x m), An = U^T A V, Bn = U^T B V in standard form.  Returns false = rejected.
+__host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n2, double* U, double* V, double* An,
+                        double* Bn) {
+  const int m = n1 + n2;
+  double anorm = 0.0, bnorm = 0.0;   // Frobenius norms of the blocks (G3)
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < m; ++r) {
+      anorm = fma(A[r + 4 * c], A[r + 4 * c], anorm);
+      bnorm = fma(B[r + 4 * c], B[r + 4 * c], bnorm);
+    }
+  anorm = sqrt(anorm);
+  bnorm = sqrt(bnorm);
+  const double eps = 2.220446049250313e-16, sml = 2.2250738585072014e-308 / 2.220446049250313e-16;
+  const double thA = fmax(20.0 * eps * anorm, sml), thB = fmax(20.0 * eps * bnorm, sml);
+  pl_eye(U, m);
+  pl_eye(V, m);
+  if (n1 == 1 && n2 == 1) {
+    // G1: V e1 along the null vector of t22 S - s22 T; U e1 along S x or T x
+    const double m11 = B[5] * A[0] - A[5] * B[0], m12 = B[5] * A[4] - A[5] * B[4];
+    double c, s, r;
+    pl_lartg(m12, -m11, c, s, r);
+    V[0] = c; V[1] = s; V[4] = -s; V[5] = c;
+    const double ax0 = A[0] * c + A[4] * s, ax1 = A[5] * s;
+    const double bx0 = B[0] * c + B[4] * s, bx1 = B[5] * s;
+    const double ra = anorm > 0.0 ? hypot(ax0, ax1) / anorm : 0.0;
+    const double rb = bnorm > 0.0 ? hypot(bx0, bx1) / bnorm : 0.0;
+    double c2, s2, r2;
+    if (ra >= rb) pl_lartg(ax0, ax1, c2, s2, r2);
+    else pl_lartg(bx0, bx1, c2, s2, r2);
+    U[0] = c2; U[1] = s2; U[4] = -s2; U[5] = c2;
+  } else {
+    // G2
+    double R[4] = {0.0, 0.0, 0.0, 0.0}, L[4] = {0.0, 0.0, 0.0, 0.0};
+    pl_gsylv(A, B, n1, n2, R, L);
+    double Mr[16], Ml[16];
+    for (int i = 0; i < 16; ++i) { Mr[i] = 0.0; Ml[i] = 0.0; }
+    for (int c = 0; c < n2; ++c) {
+      for (int r = 0; r < n1; ++r) { Mr[r + 4 * c] = -R[r + 2 * c]; Ml[r + 4 * c] = -L[r + 2 * c]; }
+      Mr[(n1 + c) + 4 * c] = 1.0;
+      Ml[(n1 + c) + 4 * c] = 1.0;
+    }
+    pl_qr_basis(Mr, m, n2, V);
+    pl_qr_basis(Ml, m, n2, U);
+  }
+  pl_congr(U, A, V, An, m);
+  pl_congr(U, B, V, Bn, m);
+  if (!(n1 == 1 && n2 == 1) && !(pl_lowfro(An, n1, n2) <= thA && pl_lowfro(Bn, n1, n2) <= thB)) {
+      // G2b: re-triangularise T's block from the left (U from the QR of (T V)(:, 1:n2)) or from
+      // the right (V completing the row space of (U^T T)(n2+1:m, :)); keep the variant whose S
+      // block below the new leading block is smaller
+      double I4[16], TV[16], UT[16], Uq[16], H[16], Vr[16], Aq[16], Ar[16];
+      pl_eye(I4, m);
+      pl_congr(I4, B, V, TV, m);
+      pl_congr(U, B, I4, UT, m);
+      double Ml[16], Mr[16];
+      for (int i = 0; i < 16; ++i) { Mr[i] = 0.0; Ml[i] = 0.0; }
+      for (int c = 0; c < n2; ++c)
+        for (int r = 0; r < m; ++r) Ml[r + 4 * c] = TV[r + 4 * c];
+      for (int c = 0; c < n1; ++c)
+        for (int r = 0; r < m; ++r) Mr[r + 4 * c] = UT[(n2 + c) + 4 * r];
+      pl_qr_basis(Ml, m, n2, Uq);
+      pl_qr_basis(Mr, m, n1, H);
+      for (int i = 0; i < 16; ++i) Vr[i] = 0.0;
+      for (int c = 0; c < n2; ++c)
+        for (int r = 0; r < m; ++r) Vr[r + 4 * c] = H[r + 4 * (n1 + c)];
+      for (int c = 0; c < n1; ++c)
+        for (int r = 0; r < m; ++r) Vr[r + 4 * (n2 + c)] = H[r + 4 * c];
+      pl_congr(Uq, A, V, Aq, m);
+      pl_congr(U, A, Vr, Ar, m);
+      double rq = 0.0, rr = 0.0;
+      for (int c = 0; c < n2; ++c)
+        for (int r = n2; r < m; ++r) { rq = fma(Aq[r + 4 * c], Aq[r + 4 * c], rq); rr = fma(Ar[r + 4 * c], Ar[r + 4 * c], rr); }
+      if (rq <= rr) { for (int i = 0; i < 16; ++i) U[i] = Uq[i]; }
+      else { for (int i = 0; i < 16; ++i) V[i] = Vr[i]; }
+    pl_congr(U, A, V, An, m);
+    pl_congr(U, B, V, Bn, m);
+  }
+  // G3
+  double resA = 0.0, resB = 0.0;
+  for (int c = 0; c < n2; ++c)
+    for (int r = n2; r < m; ++r) {
+      resA = fma(An[r + 4 * c], An[r + 4 * c], resA);
+      resB = fma(Bn[r + 4 * c], Bn[r + 4 * c], resB);
+    }
+  if (!(sqrt(resA) <= thA && sqrt(resB) <= thB)) return false;
+  for (int c = 0; c < n2; ++c)
+    for (int r = n2; r < m; ++r) { An[r + 4 * c] = 0.0; Bn[r + 4 * c] = 0.0; }
+  // G4: 2x2 blocks
+  for (int q = 0; q < 2; ++q) {
+    int p = -1;
+    if (q == 0 && n2 == 2) p = 0;
+    if (q == 1 && n1 == 2) p = n2;
+    if (p < 0) continue;
+    const double Tb[4] = {Bn[p + 4 * p], Bn[(p + 1) + 4 * p], Bn[p + 4 * (p + 1)], Bn[(p + 1) + 4 * (p + 1)]};
+    double P2[4], W2[4];
+    if (!pl_std_t22(Tb, P2, W2)) return false;
+    double Pm[16], Wm[16];
+    pl_eye(Pm, m);
+    pl_eye(Wm, m);
+    Pm[p + 4 * p] = P2[0]; Pm[(p + 1) + 4 * p] = P2[1]; Pm[p + 4 * (p + 1)] = P2[2]; Pm[(p + 1) + 4 * (p + 1)] = P2[3];
+    Wm[p + 4 * p] = W2[0]; Wm[(p + 1) + 4 * p] = W2[1]; Wm[p + 4 * (p + 1)] = W2[2]; Wm[(p + 1) + 4 * (p + 1)] = W2[3];
+    double A2[16], B2[16];
+    pl_congr(Pm, An, Wm, A2, m);
+    pl_congr(Pm, Bn, Wm, B2, m);
+    for (int i = 0; i < 16; ++i) { An[i] = A2[i]; Bn[i] = B2[i]; }
+    Bn[(p + 1) + 4 * p] = 0.0;
+    Bn[p + 4 * (p + 1)] = 0.0;
+    pl_mulr(U, Pm, m);
+    pl_mulr(V, Wm, m);
+    const double t11 = Bn[p + 4 * p], t22 = Bn[(p + 1) + 4 * (p + 1)];
+    const double e11 = An[p + 4 * p] / t11, e12 = An[p + 4 * (p + 1)] / t11;
+    const double e21 = An[(p + 1) + 4 * p] / t22, e22 = An[(p + 1) + 4 * (p + 1)] / t22;
+    const double h = 0.5 * (e11 - e22);
+    if (!(h * h + e12 * e21 < 0.0)) return false;
+  }
+  // G4: moved 1x1 blocks with t >= 0
+  for (int q = 0; q < 2; ++q) {
+    int p = -1;
+    if (q == 0 && n2 == 1) p = 0;
+    if (q == 1 && n1 == 1) p = n2;
+    if (p < 0 || !(Bn[p + 4 * p] < 0.0)) continue;
+    for (int c = 0; c < m; ++c) { An[p + 4 * c] = -An[p + 4 * c]; Bn[p + 4 * c] = -Bn[p + 4 * c]; }
+    for (int r = 0; r < m; ++r) U[r + 4 * p] = -U[r + 4 * p];
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- the window task (device)
+struct PencilWinArgs {
+  const WinDev* wins;       // this level's windows
+  int32_t nwin;
+  int32_t base;
+  const int64_t* swap_off;  // per sorted window: first swap (nw + 1 entries)
+  const int16_t* sj;        // window-local first row of each swap
+  const int8_t* s12;        // (n1 << 4) | n2
+  double* S;
+  int64_t ldS;
+  double* T;
+  int64_t ldT;
+  double* UL;               // slot arrays (kZslot doubles per slot)
+  double* VR;
+  int16_t* zrange;          // per slot (shared by UL and VR: same column structure)
+  int32_t* status;
+  int32_t* done;            // per sorted window: swaps completed
+  Control* ctl;
+  int64_t force_order;
+  int32_t force_swap;
+};
+
+__global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
+  const WinDev wd = a.wins[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int k = wd.k;
+  double* Sw = a.S + wd.j1 + wd.j1 * a.ldS;
+  double* Tw = a.T + wd.j1 + wd.j1 * a.ldT;
+  double* UL = a.UL + (int64_t)wd.slot * kZslot;
+  double* VR = a.VR + (int64_t)wd.slot * kZslot;
+  const int64_t ldS = a.ldS, ldT = a.ldT;
+  __shared__ double sU[16], sV[16], sA[16], sB[16];
+  __shared__ int16_t zlo[kZld], zhi[kZld];
+  __shared__ int s_ok;
+  for (int64_t i = tid; i < kZslot; i += blockDim.x) {
+    const int r = (int)(i % kZld), c = (int)(i / kZld);
+    const double v = (r == c && c < k) ? 1.0 : 0.0;
+    UL[i] = v;
+    VR[i] = v;
+  }
+  if (tid < kZld) {
+    zlo[tid] = (int16_t)(tid < k ? tid : kZld - 1);
+    zhi[tid] = (int16_t)(tid < k ? tid : 0);
+  }
+  __syncthreads();
+  const int64_t s0 = a.swap_off[wd.sidx], s1 = a.swap_off[wd.sidx + 1];
+  int done = 0;
+  for (int64_t s = s0; s < s1; ++s) {
+    const int j = a.sj[s], n1 = a.s12[s] >> 4, n2 = a.s12[s] & 15, m = n1 + n2;
+    if (tid == 0) {
+      double A[16], B[16], U[16], V[16], An[16], Bn[16];
+      for (int i = 0; i < 16; ++i) { A[i] = 0.0; B[i] = 0.0; }
+      for (int c = 0; c < m; ++c)
+        for (int r = 0; r < m; ++r) {
+          A[r + 4 * c] = Sw[(j + r) + (int64_t)(j + c) * ldS];
+          B[r + 4 * c] = Tw[(j + r) + (int64_t)(j + c) * ldT];
+        }
+      bool ok = pl_swap(A, B, n1, n2, U, V, An, Bn);
+      if (wd.order == a.force_order && (int)(s - s0) == a.force_swap) ok = false;
+      s_ok = ok ? 1 : 0;
+      for (int i = 0; i < 16; ++i) { sU[i] = U[i]; sV[i] = V[i]; sA[i] = An[i]; sB[i] = Bn[i]; }
+      if (ok) {
+        int lo = zlo[j], hi = zhi[j];
+        for (int c = 1; c < m; ++c) { lo = min(lo, (int)zlo[j + c]); hi = max(hi, (int)zhi[j + c]); }
+        for (int c = 0; c < m; ++c) { zlo[j + c] = (int16_t)lo; zhi[j + c] = (int16_t)hi; }
+      }
+    }
+    __syncthreads();
+    if (!s_ok) break;
+    // apply: rows j..j+m-1 right of the block (S, T); columns j..j+m-1 above it (S, T); UL, VR
+    const int nl = k - j - m, nr = j;
+    const int total = 2 * nl + 2 * nr + 2 * k;
+    for (int q = tid; q < total; q += blockDim.x) {
+      double x[4], y[4];
+      if (q < 2 * nl) {
+        const bool isT = q >= nl;
+        double* X = isT ? Tw : Sw;
+        const int64_t ld = isT ? ldT : ldS;
+        const int64_t c = j + m + (isT ? q - nl : q);
+        for (int i = 0; i < m; ++i) x[i] = X[(j + i) + c * ld];
+        for (int i = 0; i < m; ++i) {
+          double acc = 0.0;
+          for (int l = 0; l < m; ++l) acc = fma(sU[l + 4 * i], x[l], acc);
+          y[i] = acc;
+        }
+        for (int i = 0; i < m; ++i) X[(j + i) + c * ld] = y[i];
+      } else {
+        const int q2 = q - 2 * nl;
+        double* X;
+        int64_t ld;
+        int64_t r;
+        const double* F;
+        if (q2 < 2 * nr) {
+          const bool isT = q2 >= nr;
+          X = isT ? Tw : Sw; ld = isT ? ldT : ldS; r = isT ? q2 - nr : q2; F = sV;
+        } else {
+          const int q3 = q2 - 2 * nr;
+          const bool isV = q3 >= k;
+          X = isV ? VR : UL; ld = kZld; r = isV ? q3 - k : q3; F = isV ? sV : sU;
+        }
+        for (int i = 0; i < m; ++i) x[i] = X[r + (int64_t)(j + i) * ld];
+        for (int i = 0; i < m; ++i) {
+          double acc = 0.0;
+          for (int l = 0; l < m; ++l) acc = fma(x[l], F[l + 4 * i], acc);
+          y[i] = acc;
+        }
+        for (int i = 0; i < m; ++i) X[r + (int64_t)(j + i) * ld] = y[i];
+      }
+    }
+    if (tid < m * m) {
+      const int r = tid % m, c = tid / m;
+      Sw[(j + r) + (int64_t)(j + c) * ldS] = sA[r + 4 * c];
+      Tw[(j + r) + (int64_t)(j + c) * ldT] = sB[r + 4 * c];
+    }
+    ++done;
+    __syncthreads();
+  }
+  if (tid < kZld) {
+    int16_t* zr = a.zrange + (int64_t)wd.slot * kZrange;
+    zr[tid] = zlo[tid];
+    zr[kZld + tid] = zhi[tid];
+  }
+  if (tid == 0) {
+    const bool partial = done < (int)(s1 - s0);
+    a.status[wd.sidx] = partial ? kWinPartial : kWinDone;
+    a.done[wd.sidx] = done;
+    if (partial && atomicCAS(&a.ctl->abort, 0, 1) == 0) {
+      const int64_t s = s0 + done;
+      a.ctl->rej_window = wd.sidx;
+      a.ctl->rej_swaps_done = done;
+      a.ctl->rej_row = (int32_t)(wd.j1 + a.sj[s]);
+      a.ctl->rej_n1 = a.s12[s] >> 4;
+      a.ctl->rej_n2 = a.s12[s] & 15;
+    }
+  }
+}
+
+#define PK(x)                                                          \
+  do {                                                                 \
+    cudaError_t e_ = (x);                                              \
+    if (e_ != cudaSuccess) {                                           \
+      if (std::getenv("SN_DEBUG"))                                     \
+        std::fprintf(stderr, "sn: %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      rc = SN_ERR_CUDA;                                                \
+      goto done;                                                       \
+    }                                                                  \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 8); }
+};
+
+int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, int64_t ldT, double* Q, int64_t ldQ,
+               double* Zm, int64_t ldZ, int32_t* select, int64_t* m, int8_t* bmap_out, sn_stats* st,
+               cudaStream_t sA) {
+  const double t0 = now_ms();
+  int rc = 0;
+  DevBuf dsub, dbad, dwins, doff, dsj, ds12, dpref, dstatus, ddone, dctl, dUL, dVR, dzr;
+  std::vector<uint8_t> sub((size_t)n);
+  int32_t bad = 0;
+  std::vector<int8_t> bmap((size_t)n), selrow((size_t)n);
+  Plan P;
+  std::vector<int64_t> sorted, lstart;
+  std::vector<WinDev> wd;
+  std::vector<int64_t> off;
+  std::vector<int16_t> hsj;
+  std::vector<int8_t> hs12;
+  std::vector<int32_t> pref;
+  std::vector<int64_t> pref_off;
+  std::vector<int32_t> nstr;
+  std::vector<int32_t> hstatus, hdone;
+  int64_t maxper = 0, nw = 0, levels_run = 0;
+  Control hctl{};
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const int NT = 64;
+  PanelMaps mSL{}, mTL{}, mSR{}, mTR{}, mQ{}, mZ{};
+  std::memset(st, 0, sizeof(*st));
+  st->rejected_window = -1;
+  st->rejected_row = -1;
+
+  PK(dsub.alloc((size_t)n + 8));
+  PK(dbad.alloc(8));
+  PK(cudaMemsetAsync(dbad.p, 0, 4, sA));
+  launch_scan(S, ldS, n, o.validate_lower, (uint8_t*)dsub.p, (int32_t*)dbad.p, sA);
+  PK(cudaGetLastError());
+  PK(cudaMemcpyAsync(sub.data(), dsub.p, (size_t)n, cudaMemcpyDeviceToHost, sA));
+  PK(cudaMemcpyAsync(&bad, dbad.p, 4, cudaMemcpyDeviceToHost, sA));
+  PK(cudaStreamSynchronize(sA));
+  if (bad) return -2;
+  if ((rc = structure_from_sub(n, sub.data(), select, bmap.data(), selrow.data(), m))) return rc;
+  if (build_plan(n, bmap.data(), selrow.data(), o.window, o.inner_window, o.max_windows, &P)) return SN_ERR_UNSUPPORTED;
+  nw = (int64_t)P.wins.size();
+  sorted.resize(nw);
+  for (int64_t i = 0; i < nw; ++i) sorted[i] = i;
+  std::stable_sort(sorted.begin(), sorted.end(), [&](int64_t x, int64_t y) { return P.wins[x].level < P.wins[y].level; });
+  lstart.assign(P.nlevels + 1, 0);
+  for (int64_t i = 0; i < nw; ++i) lstart[P.wins[sorted[i]].level + 1]++;
+  for (int64_t l = 0; l < P.nlevels; ++l) lstart[l + 1] += lstart[l];
+  for (int64_t l = 0; l < P.nlevels; ++l) maxper = std::max(maxper, lstart[l + 1] - lstart[l]);
+  // per window: swap list (kernel execution order), descriptors; per level and kind: strips
+  wd.resize(nw);
+  off.assign(nw + 1, 0);
+  {
+    const int64_t cap = o.window * o.window / 4 + o.window + 4;
+    std::vector<int64_t> sj((size_t)cap);
+    std::vector<int8_t> a1((size_t)cap), a2((size_t)cap);
+    for (int64_t i = 0; i < nw; ++i) {
+      const WindowPlan& w = P.wins[sorted[i]];
+      const int64_t cnt = window_swaps(P, sorted[i], cap, sj.data(), a1.data(), a2.data());
+      if (cnt < 0) return SN_ERR_UNSUPPORTED;
+      for (int64_t q = 0; q < cnt; ++q) {
+        hsj.push_back((int16_t)(sj[q] - w.j1));
+        hs12.push_back((int8_t)((a1[q] << 4) | a2[q]));
+      }
+      off[i + 1] = off[i] + cnt;
+    }
+  }
+  pref_off.assign(P.nlevels * 3, 0);
+  nstr.assign(P.nlevels * 3, 0);
+  for (int64_t l = 0; l < P.nlevels; ++l) {
+    const int64_t a = lstart[l], b = lstart[l + 1];
+    for (int kind = 0; kind < 3; ++kind) {
+      pref_off[l * 3 + kind] = (int64_t)pref.size();
+      int32_t acc = 0;
+      pref.push_back(0);
+      for (int64_t i = a; i < b; ++i) {
+        const WindowPlan& w = P.wins[sorted[i]];
+        const int64_t cnt = kind == 0 ? (n - (w.j1 + w.k) + NT - 1) / NT : kind == 1 ? (w.j1 + NT - 1) / NT
+                                                                          : (n + NT - 1) / NT;
+        acc += (int32_t)cnt;
+        pref.push_back(acc);
+      }
+      nstr[l * 3 + kind] = acc;
+    }
+    for (int64_t i = a; i < b; ++i) {
+      const WindowPlan& w = P.wins[sorted[i]];
+      WinDev& d = wd[i];
+      std::memset(&d, 0, sizeof(d));
+      d.j1 = w.j1; d.k = w.k; d.nblk = w.nblk; d.ninner = w.ninner;
+      d.slot = (int32_t)(i - a);
+      d.pool = w.pool; d.order = w.order;
+      d.sidx = (int32_t)i;
+    }
+  }
+  st->ms_schedule = now_ms() - t0;
+  if (nw > 0) {
+    PK(dwins.alloc(sizeof(WinDev) * nw));
+    PK(doff.alloc(sizeof(int64_t) * (nw + 1)));
+    PK(dsj.alloc(sizeof(int16_t) * hsj.size()));
+    PK(ds12.alloc(hs12.size()));
+    PK(dpref.alloc(sizeof(int32_t) * pref.size()));
+    PK(dstatus.alloc(sizeof(int32_t) * nw));
+    PK(ddone.alloc(sizeof(int32_t) * nw));
+    PK(dctl.alloc(sizeof(Control)));
+    PK(dUL.alloc(sizeof(double) * kZslot * maxper));
+    PK(dVR.alloc(sizeof(double) * kZslot * maxper));
+    PK(dzr.alloc(sizeof(int16_t) * kZrange * maxper));
+    PK(cudaMemcpyAsync(dwins.p, wd.data(), sizeof(WinDev) * nw, cudaMemcpyHostToDevice, sA));
+    PK(cudaMemcpyAsync(doff.p, off.data(), sizeof(int64_t) * (nw + 1), cudaMemcpyHostToDevice, sA));
+    if (!hsj.empty()) {
+      PK(cudaMemcpyAsync(dsj.p, hsj.data(), sizeof(int16_t) * hsj.size(), cudaMemcpyHostToDevice, sA));
+      PK(cudaMemcpyAsync(ds12.p, hs12.data(), hs12.size(), cudaMemcpyHostToDevice, sA));
+    }
+    PK(cudaMemcpyAsync(dpref.p, pref.data(), sizeof(int32_t) * pref.size(), cudaMemcpyHostToDevice, sA));
+    PK(cudaMemsetAsync(dstatus.p, 0, sizeof(int32_t) * nw, sA));
+    PK(cudaMemsetAsync(ddone.p, 0, sizeof(int32_t) * nw, sA));
+    PK(cudaMemsetAsync(dctl.p, 0, sizeof(Control), sA));
+    // TMA descriptors: S and T against UL (left) and VR (right), Q against UL, Z against VR
+    panel_maps_init(&mSL, (double*)dUL.p, maxper, S, n, n, ldS);
+    panel_maps_init(&mTL, (double*)dUL.p, maxper, T, n, n, ldT);
+    panel_maps_init(&mSR, (double*)dVR.p, maxper, S, n, n, ldS);
+    panel_maps_init(&mTR, (double*)dVR.p, maxper, T, n, n, ldT);
+    if (Q) panel_maps_init(&mQ, (double*)dUL.p, maxper, Q, n, n, ldQ);
+    if (Zm) panel_maps_init(&mZ, (double*)dVR.p, maxper, Zm, n, n, ldZ);
+    PK(cudaEventCreate(&e0));
+    PK(cudaEventCreate(&e1));
+    PK(cudaEventRecord(e0, sA));
+    const int mt = o.window <= 64 ? 64 : (o.window <= 128 ? 128 : 256);
+    for (int64_t l = 0; l < P.nlevels; ++l) {
+      const int64_t a = lstart[l], b = lstart[l + 1];
+      PencilWinArgs wa{};
+      wa.wins = (const WinDev*)dwins.p + a; wa.nwin = (int32_t)(b - a); wa.base = (int32_t)a;
+      wa.swap_off = (const int64_t*)doff.p; wa.sj = (const int16_t*)dsj.p; wa.s12 = (const int8_t*)ds12.p;
+      wa.S = S; wa.ldS = ldS; wa.T = T; wa.ldT = ldT;
+      wa.UL = (double*)dUL.p; wa.VR = (double*)dVR.p; wa.zrange = (int16_t*)dzr.p;
+      wa.status = (int32_t*)dstatus.p; wa.done = (int32_t*)ddone.p; wa.ctl = (Control*)dctl.p;
+      wa.force_order = o.force_reject_window; wa.force_swap = (int32_t)o.force_reject_swap;
+      pencil_window_kernel<<<(unsigned)(b - a), 256, 0, sA>>>(wa);
+      PK(cudaGetLastError());
+      st->launches[0]++;
+      auto panel = [&](int kind, double* M, int64_t ld, const double* Zs, const PanelMaps* pm) {
+        const int32_t ns = nstr[l * 3 + kind];
+        if (ns <= 0 || M == nullptr) return;
+        PanelArgs pa{};
+        pa.wins = (const WinDev*)dwins.p + a; pa.nwin = (int32_t)(b - a); pa.base = (int32_t)a;
+        pa.prefix = (const int32_t*)dpref.p + pref_off[l * 3 + kind];
+        pa.strips = nullptr; pa.nseg = 0; pa.part = 0;
+        pa.vec16 = (((uintptr_t)M & 15) == 0 && (ld % 2) == 0) ? 1 : 0;
+        pa.status = (const int32_t*)dstatus.p;
+        pa.M = M; pa.ld = ld; pa.n = n; pa.Z = Zs; pa.zrange = (const int16_t*)dzr.p;
+        pa.maps = pm;
+        launch_panel(kind, mt, pa, ns, sA);
+        st->launches[kind + 1]++;
+      };
+      panel(0, S, ldS, (double*)dUL.p, &mSL);
+      panel(0, T, ldT, (double*)dUL.p, &mTL);
+      panel(1, S, ldS, (double*)dVR.p, &mSR);
+      panel(1, T, ldT, (double*)dVR.p, &mTR);
+      panel(2, Q, ldQ, (double*)dUL.p, &mQ);
+      panel(2, Zm, ldZ, (double*)dVR.p, &mZ);
+      PK(cudaGetLastError());
+      levels_run = l + 1;
+      // a rejection stops the run after this level (its panels apply the partial factors)
+      int32_t abort_flag = 0;
+      PK(cudaMemcpyAsync(&abort_flag, dctl.p, sizeof(int32_t), cudaMemcpyDeviceToHost, sA));
+      PK(cudaStreamSynchronize(sA));
+      if (abort_flag) break;
+    }
+    PK(cudaEventRecord(e1, sA));
+    PK(cudaEventSynchronize(e1));
+    float ms = 0.0f;
+    PK(cudaEventElapsedTime(&ms, e0, e1));
+    st->ms_device = ms;
+    hstatus.resize(nw);
+    hdone.resize(nw);
+    PK(cudaMemcpy(hstatus.data(), dstatus.p, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
+    PK(cudaMemcpy(hdone.data(), ddone.p, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
+    PK(cudaMemcpy(&hctl, dctl.p, sizeof(Control), cudaMemcpyDeviceToHost));
+  }
+  {
+    // final block list: replay the executed swaps on the initial list (block at each first row)
+    std::vector<int8_t> bsz((size_t)n + 2, 0), bsel((size_t)n + 2, 0);   // indexed by first row
+    for (int64_t i = 0; i < n;) {
+      const int sz = bmap[i] == 1 ? 2 : 1;
+      bsz[i] = (int8_t)sz;
+      bsel[i] = selrow[i];
+      i += sz;
+    }
+    int64_t executed = 0, swaps = 0;
+    for (int64_t i = 0; i < lstart[levels_run]; ++i) {
+      if (hstatus.empty() || hstatus[i] == kWinSkipped) continue;
+      const WindowPlan& w = P.wins[sorted[i]];
+      ++executed;
+      const int64_t cnt = hstatus[i] == kWinDone ? off[i + 1] - off[i] : hdone[i];
+      for (int64_t q = 0; q < cnt; ++q) {
+        const int64_t j = w.j1 + hsj[off[i] + q];
+        const int n1 = hs12[off[i] + q] >> 4, n2 = hs12[off[i] + q] & 15;
+        const int8_t sel1 = bsel[j], sel2 = bsel[j + n1];
+        bsz[j] = 0; bsz[j + n1] = 0;
+        bsz[j] = (int8_t)n2; bsel[j] = sel2;
+        bsz[j + n2] = (int8_t)n1; bsel[j + n2] = sel1;
+        st->swaps_by_type[(n1 - 1) * 2 + (n2 - 1)]++;
+      }
+      swaps += cnt;
+      const double k = w.k;
+      st->eq_flops += 2.0 * k * k * (2.0 * (double)(n - w.j1 - w.k) + 2.0 * (double)w.j1 + (Q ? (double)n : 0.0) +
+                                     (Zm ? (double)n : 0.0));
+    }
+    for (int64_t i = 0; i < n;) {
+      const int sz = bsz[i];
+      for (int q = 0; q < sz; ++q) {
+        select[i + q] = bsel[i];
+        if (bmap_out) bmap_out[i + q] = (int8_t)(sz == 1 ? 0 : 1 + q);
+      }
+      i += sz;
+    }
+    st->windows = executed;
+    st->swaps = swaps;
+    st->levels = P.nlevels;
+    if (hctl.abort) {
+      rc = SN_ERR_REJECTED;
+      st->rejected_window = P.wins[sorted[hctl.rej_window]].order;
+      st->rejected_row = hctl.rej_row;
+      st->rejected_n1 = hctl.rej_n1;
+      st->rejected_n2 = hctl.rej_n2;
+    }
+  }
+  st->ms_total = now_ms() - t0;
+done:
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  return rc;
+}
+
+}  // namespace
+}  // namespace sn
+
+extern "C" int sn_reorder_pencil_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS, double* T, int64_t ldT,
+                                    double* Q, int64_t ldQ, double* Z, int64_t ldZ, int32_t* select, int64_t* m,
+                                    int8_t* bmap_out, sn_stats* stats, void* stream) {
+  using namespace sn;
+  sn_opts o;
+  if (opts) o = *opts;
+  else sn_default_opts(&o);
+  if (n < 0) return -2;
+  if (m == nullptr) return -12;
+  *m = 0;
+  if (n == 0) return 0;
+  if (!S) return -3;
+  if (ldS < n) return -4;
+  if (!T) return -5;
+  if (ldT < n) return -6;
+  if (Q && ldQ < n) return -8;
+  if (Z && ldZ < n) return -10;
+  if (!select) return -11;
+  if (o.window < 4 || o.window > 256 || o.inner_window < 4 || o.inner_window > kInner) return SN_ERR_UNSUPPORTED;
+  if (!is_device_ptr(S) || !is_device_ptr(T) || (Q && !is_device_ptr(Q)) || (Z && !is_device_ptr(Z)))
+    return SN_ERR_UNSUPPORTED;   // device pointers only (this version)
+  std::lock_guard<std::mutex> lock(g_mu);
+  sn_stats local;
+  sn_stats* st = stats ? stats : &local;
+  return run_pencil(o, n, S, ldS, T, ldT, Q, ldQ, Z, ldZ, select, m, bmap_out, st, (cudaStream_t)stream);
+}
