@@ -212,7 +212,7 @@ __host__ __device__ bool pl_std_t22(const double* Tb, double* P, double* W) {
 // The transform of one swap (G1-G4).  A, B: the m x m blocks of S and T (ld 4, m = n1 + n2).
 // Out: U, V (m x m), An = U^T A V, Bn = U^T B V in standard form.  Returns false = rejected.
 __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n2, double* U, double* V, double* An,
-                        double* Bn) {
+                        double* Bn, double* why = nullptr) {
   const int m = n1 + n2;
   double anorm = 0.0, bnorm = 0.0;   // Frobenius norms of the blocks (G3)
   for (int c = 0; c < m; ++c)
@@ -294,7 +294,10 @@ __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n
       resA = fma(An[r + 4 * c], An[r + 4 * c], resA);
       resB = fma(Bn[r + 4 * c], Bn[r + 4 * c], resB);
     }
-  if (!(sqrt(resA) <= thA && sqrt(resB) <= thB)) return false;
+  if (!(sqrt(resA) <= thA && sqrt(resB) <= thB)) {
+    if (why) { why[0] = 1.0; why[1] = fmax(sqrt(resA) / thA, sqrt(resB) / thB); }
+    return false;
+  }
   for (int c = 0; c < n2; ++c)
     for (int r = n2; r < m; ++r) { An[r + 4 * c] = 0.0; Bn[r + 4 * c] = 0.0; }
   // G4: 2x2 blocks
@@ -305,7 +308,10 @@ __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n
     if (p < 0) continue;
     const double Tb[4] = {Bn[p + 4 * p], Bn[(p + 1) + 4 * p], Bn[p + 4 * (p + 1)], Bn[(p + 1) + 4 * (p + 1)]};
     double P2[4], W2[4];
-    if (!pl_std_t22(Tb, P2, W2)) return false;
+    if (!pl_std_t22(Tb, P2, W2)) {
+      if (why) { why[0] = 2.0; why[1] = 0.0; }
+      return false;
+    }
     double Pm[16], Wm[16];
     pl_eye(Pm, m);
     pl_eye(Wm, m);
@@ -323,7 +329,10 @@ __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n
     const double e11 = An[p + 4 * p] / t11, e12 = An[p + 4 * (p + 1)] / t11;
     const double e21 = An[(p + 1) + 4 * p] / t22, e22 = An[(p + 1) + 4 * (p + 1)] / t22;
     const double h = 0.5 * (e11 - e22);
-    if (!(h * h + e12 * e21 < 0.0)) return false;
+    if (!(h * h + e12 * e21 < 0.0)) {
+      if (why) { why[0] = 3.0; why[1] = h * h + e12 * e21; }
+      return false;
+    }
   }
   // G4: moved 1x1 blocks with t >= 0
   for (int q = 0; q < 2; ++q) {
@@ -371,6 +380,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   __shared__ double sU[16], sV[16], sA[16], sB[16];
   __shared__ int16_t zlo[kZld], zhi[kZld];
   __shared__ int s_ok;
+  __shared__ double s_why[2];
   for (int64_t i = tid; i < kZslot; i += blockDim.x) {
     const int r = (int)(i % kZld), c = (int)(i / kZld);
     const double v = (r == c && c < k) ? 1.0 : 0.0;
@@ -394,7 +404,9 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
           A[r + 4 * c] = Sw[(j + r) + (int64_t)(j + c) * ldS];
           B[r + 4 * c] = Tw[(j + r) + (int64_t)(j + c) * ldT];
         }
-      bool ok = pl_swap(A, B, n1, n2, U, V, An, Bn);
+      double why[2] = {0.0, 0.0};
+      bool ok = pl_swap(A, B, n1, n2, U, V, An, Bn, why);
+      if (!ok) { s_why[0] = why[0]; s_why[1] = why[1]; }
       if (wd.order == a.force_order && (int)(s - s0) == a.force_swap) ok = false;
       s_ok = ok ? 1 : 0;
       for (int i = 0; i < 16; ++i) { sU[i] = U[i]; sV[i] = V[i]; sA[i] = An[i]; sB[i] = Bn[i]; }
@@ -470,6 +482,8 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       a.ctl->rej_row = (int32_t)(wd.j1 + a.sj[s]);
       a.ctl->rej_n1 = a.s12[s] >> 4;
       a.ctl->rej_n2 = a.s12[s] & 15;
+      a.ctl->pad[0] = (int32_t)s_why[0];                       // failed test: 1 G3, 2/3 G4
+      a.ctl->pad[1] = (int32_t)fmin(s_why[1] * 1000.0, 2e9);   // G3: residual / threshold x 1000
     }
   }
 }
@@ -710,6 +724,10 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
     st->levels = P.nlevels;
     if (hctl.abort) {
       rc = SN_ERR_REJECTED;
+      if (std::getenv("SN_DEBUG"))
+        std::fprintf(stderr, "sn pencil: rejected window %d (order %lld) swap %d row %d (%d|%d): test %d ratio %.3f\n",
+                     hctl.rej_window, (long long)P.wins[sorted[hctl.rej_window]].order, hctl.rej_swaps_done,
+                     hctl.rej_row, hctl.rej_n1, hctl.rej_n2, hctl.pad[0], hctl.pad[1] / 1000.0);
       st->rejected_window = P.wins[sorted[hctl.rej_window]].order;
       st->rejected_row = hctl.rej_row;
       st->rejected_n1 = hctl.rej_n1;
