@@ -12,10 +12,11 @@
 // weak stability test; T's 2x2 blocks diagonal with t11 >= t22 > 0 by a 2x2 SVD; moved 1x1
 // blocks with t >= 0).
 //
-// First version (correctness first): one CTA per window, one thread evaluates each swap's
-// transform, 256 threads apply it to the window of S and T (in place in global memory, L2
-// resident) and to UL / VR; the column nonzero intervals of the accumulators are tracked as
-// in the standard window kernel so the panel kernels skip structural zeros.
+// Window task: one CTA per window; the swaps run in steps of swaps on disjoint rows (one
+// thread per swap computes its transform, 256 threads apply them to the window of S and T in
+// place in global memory -- L2 resident -- and to UL / VR); the column nonzero intervals of the
+// accumulators are tracked as in the standard window kernel so the panel kernels skip
+// structural zeros.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -347,13 +348,25 @@ __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n
 }
 
 // ---------------------------------------------------------------- the window task (device)
+// The swaps of a window run in steps: the host assigns each swap (in the order of the standard
+// kernel's swap list) the step after the last earlier swap whose rows it overlaps, so the
+// swaps of one step act on pairwise disjoint row ranges.  Such swaps commute exactly (their
+// left and right transforms touch disjoint rows / columns, and none touches another's
+// diagonal block), so one step is: every swap's transform from the current blocks (one thread
+// each), then all row applications, then all column applications.  A step with a rejected swap
+// is not applied (the window stops after the previous step, a closed set of swaps).
+constexpr int kRecD = 64;   // doubles per swap record in shared memory: U, V, An, Bn (4x4 each)
+
 struct PencilWinArgs {
   const WinDev* wins;       // this level's windows
   int32_t nwin;
   int32_t base;
-  const int64_t* swap_off;  // per sorted window: first swap (nw + 1 entries)
+  const int64_t* swap_off;  // per sorted window: first swap (nw + 1 entries), step-sorted
+  const int32_t* step_off;  // per sorted window: steps at step_base[sidx] .. (+ nsteps + 1)
+  const int64_t* step_base;
   const int16_t* sj;        // window-local first row of each swap
   const int8_t* s12;        // (n1 << 4) | n2
+  const int32_t* sidx;      // index of each swap in the window's list order
   double* S;
   int64_t ldS;
   double* T;
@@ -362,13 +375,24 @@ struct PencilWinArgs {
   double* VR;
   int16_t* zrange;          // per slot (shared by UL and VR: same column structure)
   int32_t* status;
-  int32_t* done;            // per sorted window: swaps completed
+  int32_t* done;            // per sorted window: swaps completed (a prefix of the step-sorted list)
   Control* ctl;
   int64_t force_order;
   int32_t force_swap;
 };
 
+// index i with pre[i] <= q < pre[i + 1]
+__device__ __forceinline__ int pl_find(const int* pre, int cnt, int q) {
+  int lo = 0, hi = cnt - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= q) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
+  extern __shared__ double rec[];            // kRecD doubles per swap of the current step
   const WinDev wd = a.wins[blockIdx.x];
   const int tid = threadIdx.x;
   const int k = wd.k;
@@ -377,9 +401,9 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   double* UL = a.UL + (int64_t)wd.slot * kZslot;
   double* VR = a.VR + (int64_t)wd.slot * kZslot;
   const int64_t ldS = a.ldS, ldT = a.ldT;
-  __shared__ double sU[16], sV[16], sA[16], sB[16];
   __shared__ int16_t zlo[kZld], zhi[kZld];
-  __shared__ int s_ok;
+  __shared__ int s_pre[kZld + 1];
+  __shared__ int s_rej;
   __shared__ double s_why[2];
   for (int64_t i = tid; i < kZslot; i += blockDim.x) {
     const int r = (int)(i % kZld), c = (int)(i / kZld);
@@ -391,98 +415,140 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     zlo[tid] = (int16_t)(tid < k ? tid : kZld - 1);
     zhi[tid] = (int16_t)(tid < k ? tid : 0);
   }
+  if (tid == 0) s_rej = 0x7fffffff;
   __syncthreads();
-  const int64_t s0 = a.swap_off[wd.sidx], s1 = a.swap_off[wd.sidx + 1];
-  int done = 0;
-  for (int64_t s = s0; s < s1; ++s) {
-    const int j = a.sj[s], n1 = a.s12[s] >> 4, n2 = a.s12[s] & 15, m = n1 + n2;
-    if (tid == 0) {
-      double A[16], B[16], U[16], V[16], An[16], Bn[16];
+  const int64_t s0 = a.swap_off[wd.sidx];
+  const int32_t* soff = a.step_off + a.step_base[wd.sidx];
+  const int nsteps = (int)(a.step_base[wd.sidx + 1] - a.step_base[wd.sidx]) - 1;
+  int done_steps = 0;
+  for (int st = 0; st < nsteps; ++st) {
+    const int b0 = soff[st], cnt = soff[st + 1] - b0;
+    // (1) transforms, one thread per swap
+    if (tid < cnt) {
+      const int64_t s = s0 + b0 + tid;
+      const int j = a.sj[s], n1 = a.s12[s] >> 4, n2 = a.s12[s] & 15, m = n1 + n2;
+      double A[16], B[16];
       for (int i = 0; i < 16; ++i) { A[i] = 0.0; B[i] = 0.0; }
       for (int c = 0; c < m; ++c)
         for (int r = 0; r < m; ++r) {
           A[r + 4 * c] = Sw[(j + r) + (int64_t)(j + c) * ldS];
           B[r + 4 * c] = Tw[(j + r) + (int64_t)(j + c) * ldT];
         }
+      double* R = rec + tid * kRecD;
       double why[2] = {0.0, 0.0};
-      bool ok = pl_swap(A, B, n1, n2, U, V, An, Bn, why);
-      if (!ok) { s_why[0] = why[0]; s_why[1] = why[1]; }
-      if (wd.order == a.force_order && (int)(s - s0) == a.force_swap) ok = false;
-      s_ok = ok ? 1 : 0;
-      for (int i = 0; i < 16; ++i) { sU[i] = U[i]; sV[i] = V[i]; sA[i] = An[i]; sB[i] = Bn[i]; }
-      if (ok) {
-        int lo = zlo[j], hi = zhi[j];
-        for (int c = 1; c < m; ++c) { lo = min(lo, (int)zlo[j + c]); hi = max(hi, (int)zhi[j + c]); }
-        for (int c = 0; c < m; ++c) { zlo[j + c] = (int16_t)lo; zhi[j + c] = (int16_t)hi; }
+      bool ok = pl_swap(A, B, n1, n2, R, R + 16, R + 32, R + 48, why);
+      if (wd.order == a.force_order && a.sidx[s] == a.force_swap) { ok = false; why[0] = 0.0; }
+      if (!ok) {
+        const int key = a.sidx[s];
+        if (atomicMin(&s_rej, key) > key) { s_why[0] = why[0]; s_why[1] = why[1]; }
       }
     }
     __syncthreads();
-    if (!s_ok) break;
-    // apply: rows j..j+m-1 right of the block (S, T); columns j..j+m-1 above it (S, T); UL, VR
-    const int nl = k - j - m, nr = j;
-    const int total = 2 * nl + 2 * nr + 2 * k;
-    for (int q = tid; q < total; q += blockDim.x) {
-      double x[4], y[4];
-      if (q < 2 * nl) {
-        const bool isT = q >= nl;
-        double* X = isT ? Tw : Sw;
-        const int64_t ld = isT ? ldT : ldS;
-        const int64_t c = j + m + (isT ? q - nl : q);
-        for (int i = 0; i < m; ++i) x[i] = X[(j + i) + c * ld];
-        for (int i = 0; i < m; ++i) {
-          double acc = 0.0;
-          for (int l = 0; l < m; ++l) acc = fma(sU[l + 4 * i], x[l], acc);
-          y[i] = acc;
-        }
-        for (int i = 0; i < m; ++i) X[(j + i) + c * ld] = y[i];
-      } else {
-        const int q2 = q - 2 * nl;
-        double* X;
-        int64_t ld;
-        int64_t r;
-        const double* F;
-        if (q2 < 2 * nr) {
-          const bool isT = q2 >= nr;
-          X = isT ? Tw : Sw; ld = isT ? ldT : ldS; r = isT ? q2 - nr : q2; F = sV;
-        } else {
-          const int q3 = q2 - 2 * nr;
-          const bool isV = q3 >= k;
-          X = isV ? VR : UL; ld = kZld; r = isV ? q3 - k : q3; F = isV ? sV : sU;
-        }
-        for (int i = 0; i < m; ++i) x[i] = X[r + (int64_t)(j + i) * ld];
-        for (int i = 0; i < m; ++i) {
-          double acc = 0.0;
-          for (int l = 0; l < m; ++l) acc = fma(x[l], F[l + 4 * i], acc);
-          y[i] = acc;
-        }
-        for (int i = 0; i < m; ++i) X[r + (int64_t)(j + i) * ld] = y[i];
+    if (s_rej != 0x7fffffff) break;
+    // (2) column intervals of the accumulators; row-application task counts
+    if (tid < cnt) {
+      const int64_t s = s0 + b0 + tid;
+      const int j = a.sj[s], m = (a.s12[s] >> 4) + (a.s12[s] & 15);
+      int lo = zlo[j], hi = zhi[j];
+      for (int c = 1; c < m; ++c) { lo = min(lo, (int)zlo[j + c]); hi = max(hi, (int)zhi[j + c]); }
+      for (int c = 0; c < m; ++c) { zlo[j + c] = (int16_t)lo; zhi[j + c] = (int16_t)hi; }
+    }
+    if (tid == 0) {
+      s_pre[0] = 0;
+      for (int i = 0; i < cnt; ++i) {
+        const int64_t s = s0 + b0 + i;
+        const int j = a.sj[s], m = (a.s12[s] >> 4) + (a.s12[s] & 15);
+        s_pre[i + 1] = s_pre[i] + 2 * (k - j - m) + m * m;
       }
     }
-    if (tid < m * m) {
-      const int r = tid % m, c = tid / m;
-      Sw[(j + r) + (int64_t)(j + c) * ldS] = sA[r + 4 * c];
-      Tw[(j + r) + (int64_t)(j + c) * ldT] = sB[r + 4 * c];
+    __syncthreads();
+    // (3) rows j..j+m-1 right of each block (S, T) and the new diagonal blocks
+    for (int q = tid; q < s_pre[cnt]; q += blockDim.x) {
+      const int i = pl_find(s_pre, cnt, q);
+      const int64_t s = s0 + b0 + i;
+      const int j = a.sj[s], m = (a.s12[s] >> 4) + (a.s12[s] & 15);
+      const double* R = rec + i * kRecD;
+      const int nl = k - j - m, e = q - s_pre[i];
+      if (e >= 2 * nl) {
+        const int d = e - 2 * nl, r = d % m, c = d / m;
+        Sw[(j + r) + (int64_t)(j + c) * ldS] = R[32 + r + 4 * c];
+        Tw[(j + r) + (int64_t)(j + c) * ldT] = R[48 + r + 4 * c];
+        continue;
+      }
+      const bool isT = e >= nl;
+      double* X = isT ? Tw : Sw;
+      const int64_t ld = isT ? ldT : ldS;
+      const int64_t c = j + m + (isT ? e - nl : e);
+      double x[4], y[4];
+      for (int t = 0; t < m; ++t) x[t] = X[(j + t) + c * ld];
+      for (int t = 0; t < m; ++t) {
+        double acc = 0.0;
+        for (int l = 0; l < m; ++l) acc = fma(R[l + 4 * t], x[l], acc);
+        y[t] = acc;
+      }
+      for (int t = 0; t < m; ++t) X[(j + t) + c * ld] = y[t];
     }
-    ++done;
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = 0; i < cnt; ++i) {
+        const int64_t s = s0 + b0 + i;
+        const int j = a.sj[s];
+        s_pre[i + 1] = s_pre[i] + 2 * j + 2 * k;
+      }
+    }
+    __syncthreads();
+    // (4) columns j..j+m-1 above each block (S, T) and of UL, VR
+    for (int q = tid; q < s_pre[cnt]; q += blockDim.x) {
+      const int i = pl_find(s_pre, cnt, q);
+      const int64_t s = s0 + b0 + i;
+      const int j = a.sj[s], m = (a.s12[s] >> 4) + (a.s12[s] & 15);
+      const double* R = rec + i * kRecD;
+      const int e = q - s_pre[i];
+      double* X;
+      int64_t ld, r;
+      const double* F;
+      if (e < 2 * j) {
+        const bool isT = e >= j;
+        X = isT ? Tw : Sw; ld = isT ? ldT : ldS; r = isT ? e - j : e; F = R + 16;
+      } else {
+        const int e3 = e - 2 * j;
+        const bool isV = e3 >= k;
+        X = isV ? VR : UL; ld = kZld; r = isV ? e3 - k : e3; F = isV ? R + 16 : R;
+      }
+      double x[4], y[4];
+      for (int t = 0; t < m; ++t) x[t] = X[r + (int64_t)(j + t) * ld];
+      for (int t = 0; t < m; ++t) {
+        double acc = 0.0;
+        for (int l = 0; l < m; ++l) acc = fma(x[l], F[l + 4 * t], acc);
+        y[t] = acc;
+      }
+      for (int t = 0; t < m; ++t) X[r + (int64_t)(j + t) * ld] = y[t];
+    }
+    done_steps = st + 1;
     __syncthreads();
   }
+  const int done = soff[done_steps] - soff[0];
+  const int total = soff[nsteps] - soff[0];
   if (tid < kZld) {
     int16_t* zr = a.zrange + (int64_t)wd.slot * kZrange;
     zr[tid] = zlo[tid];
     zr[kZld + tid] = zhi[tid];
   }
   if (tid == 0) {
-    const bool partial = done < (int)(s1 - s0);
+    const bool partial = done < total;
     a.status[wd.sidx] = partial ? kWinPartial : kWinDone;
     a.done[wd.sidx] = done;
     if (partial && atomicCAS(&a.ctl->abort, 0, 1) == 0) {
-      const int64_t s = s0 + done;
+      // the rejecting swap with the smallest list index in the failed step
+      int64_t s = s0 + done;
+      for (int64_t q = s0 + soff[done_steps]; q < s0 + soff[done_steps + 1]; ++q)
+        if (a.sidx[q] == s_rej) s = q;
       a.ctl->rej_window = wd.sidx;
       a.ctl->rej_swaps_done = done;
       a.ctl->rej_row = (int32_t)(wd.j1 + a.sj[s]);
       a.ctl->rej_n1 = a.s12[s] >> 4;
       a.ctl->rej_n2 = a.s12[s] & 15;
-      a.ctl->pad[0] = (int32_t)s_why[0];                       // failed test: 1 G3, 2/3 G4
+      a.ctl->pad[0] = (int32_t)s_why[0];                       // failed test: 1 G3, 2/3 G4, 0 forced
       a.ctl->pad[1] = (int32_t)fmin(s_why[1] * 1000.0, 2e9);   // G3: residual / threshold x 1000
     }
   }
@@ -510,7 +576,7 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
                cudaStream_t sA) {
   const double t0 = now_ms();
   int rc = 0;
-  DevBuf dsub, dbad, dwins, doff, dsj, ds12, dpref, dstatus, ddone, dctl, dUL, dVR, dzr;
+  DevBuf dsub, dbad, dwins, doff, dsj, ds12, dpref, dstatus, ddone, dctl, dUL, dVR, dzr, dstep, dstepb, didx;
   std::vector<uint8_t> sub((size_t)n);
   int32_t bad = 0;
   std::vector<int8_t> bmap((size_t)n), selrow((size_t)n);
@@ -520,6 +586,9 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
   std::vector<int64_t> off;
   std::vector<int16_t> hsj;
   std::vector<int8_t> hs12;
+  std::vector<int32_t> hidx, hstep;
+  std::vector<int64_t> hstep_base;
+  int max_step_cnt = 1;
   std::vector<int32_t> pref;
   std::vector<int64_t> pref_off;
   std::vector<int32_t> nstr;
@@ -563,9 +632,36 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
       const WindowPlan& w = P.wins[sorted[i]];
       const int64_t cnt = window_swaps(P, sorted[i], cap, sj.data(), a1.data(), a2.data());
       if (cnt < 0) return SN_ERR_UNSUPPORTED;
+      // steps: each swap goes one step after the last earlier swap overlapping its rows
+      std::vector<int32_t> last((size_t)w.k + 4, -1), stp((size_t)cnt);
+      int32_t ns = 0;
       for (int64_t q = 0; q < cnt; ++q) {
-        hsj.push_back((int16_t)(sj[q] - w.j1));
-        hs12.push_back((int8_t)((a1[q] << 4) | a2[q]));
+        const int64_t j = sj[q] - w.j1;
+        const int mm = a1[q] + a2[q];
+        int32_t t = 0;
+        for (int r = 0; r < mm; ++r) t = std::max(t, last[j + r] + 1);
+        for (int r = 0; r < mm; ++r) last[j + r] = t;
+        stp[q] = t;
+        ns = std::max(ns, t + 1);
+      }
+      std::vector<int32_t> per((size_t)ns + 1, 0);
+      for (int64_t q = 0; q < cnt; ++q) per[stp[q] + 1]++;
+      for (int32_t t = 0; t < ns; ++t) {
+        max_step_cnt = std::max(max_step_cnt, per[t + 1]);
+        per[t + 1] += per[t];
+      }
+      hstep_base.push_back((int64_t)hstep.size());
+      for (int32_t t = 0; t <= ns; ++t) hstep.push_back(per[t]);
+      std::vector<int64_t> ord((size_t)cnt);
+      {
+        std::vector<int32_t> fill(per.begin(), per.end() - 1);
+        for (int64_t q = 0; q < cnt; ++q) ord[fill[stp[q]]++] = q;   // stable within a step
+      }
+      for (int64_t q = 0; q < cnt; ++q) {
+        const int64_t o = ord[q];
+        hsj.push_back((int16_t)(sj[o] - w.j1));
+        hs12.push_back((int8_t)((a1[o] << 4) | a2[o]));
+        hidx.push_back((int32_t)o);
       }
       off[i + 1] = off[i] + cnt;
     }
@@ -601,6 +697,14 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
   if (nw > 0) {
     PK(dwins.alloc(sizeof(WinDev) * nw));
     PK(doff.alloc(sizeof(int64_t) * (nw + 1)));
+    hstep_base.push_back((int64_t)hstep.size());
+    PK(dstep.alloc(sizeof(int32_t) * hstep.size()));
+    PK(dstepb.alloc(sizeof(int64_t) * hstep_base.size()));
+    PK(didx.alloc(sizeof(int32_t) * (hidx.size() + 1)));
+    PK(cudaMemcpyAsync(dstep.p, hstep.data(), sizeof(int32_t) * hstep.size(), cudaMemcpyHostToDevice, sA));
+    PK(cudaMemcpyAsync(dstepb.p, hstep_base.data(), sizeof(int64_t) * hstep_base.size(), cudaMemcpyHostToDevice, sA));
+    if (!hidx.empty())
+      PK(cudaMemcpyAsync(didx.p, hidx.data(), sizeof(int32_t) * hidx.size(), cudaMemcpyHostToDevice, sA));
     PK(dsj.alloc(sizeof(int16_t) * hsj.size()));
     PK(ds12.alloc(hs12.size()));
     PK(dpref.alloc(sizeof(int32_t) * pref.size()));
@@ -631,16 +735,21 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
     PK(cudaEventCreate(&e1));
     PK(cudaEventRecord(e0, sA));
     const int mt = o.window <= 64 ? 64 : (o.window <= 128 ? 128 : 256);
+    const size_t smem_rec = sizeof(double) * kRecD * (size_t)max_step_cnt;
+    if (max_step_cnt > 256) { rc = SN_ERR_UNSUPPORTED; goto done; }
+    PK(cudaFuncSetAttribute(pencil_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rec));
     for (int64_t l = 0; l < P.nlevels; ++l) {
       const int64_t a = lstart[l], b = lstart[l + 1];
       PencilWinArgs wa{};
       wa.wins = (const WinDev*)dwins.p + a; wa.nwin = (int32_t)(b - a); wa.base = (int32_t)a;
       wa.swap_off = (const int64_t*)doff.p; wa.sj = (const int16_t*)dsj.p; wa.s12 = (const int8_t*)ds12.p;
+      wa.step_off = (const int32_t*)dstep.p; wa.step_base = (const int64_t*)dstepb.p;
+      wa.sidx = (const int32_t*)didx.p;
       wa.S = S; wa.ldS = ldS; wa.T = T; wa.ldT = ldT;
       wa.UL = (double*)dUL.p; wa.VR = (double*)dVR.p; wa.zrange = (int16_t*)dzr.p;
       wa.status = (int32_t*)dstatus.p; wa.done = (int32_t*)ddone.p; wa.ctl = (Control*)dctl.p;
       wa.force_order = o.force_reject_window; wa.force_swap = (int32_t)o.force_reject_swap;
-      pencil_window_kernel<<<(unsigned)(b - a), 256, 0, sA>>>(wa);
+      pencil_window_kernel<<<(unsigned)(b - a), 256, smem_rec, sA>>>(wa);
       PK(cudaGetLastError());
       st->launches[0]++;
       auto panel = [&](int kind, double* M, int64_t ld, const double* Zs, const PanelMaps* pm) {
