@@ -309,3 +309,30 @@ def test_greorder_argument_errors():
     assert oracle.greorder(S, T, Q, Z, p.select, w=3)["rc"] == -13
     r = oracle.greorder(S, T, None, None, p.select, w=8)
     assert r["rc"] == 0
+
+
+def test_greorder_inwindow_order_independence():
+    # reading R12 for pencils: the GPU executes each window's swaps in the product's order
+    # (inner windows, movers top to bottom; sn_schedule_window_swaps, host code) -- the same
+    # block pairs as the oracle's mover-by-mover order.  Applying the oracle's own swap in that
+    # order must give the oracle's result to rounding, up to basis-vector signs.
+    import ctypes as C
+    import paper_1905_04975_b200 as sn
+    p = make_pencil(160, p2=0.25, q="householder", psel=0.4, w=32, seed=21)
+    S, T, Q, Z = (p.np(x).copy(order="F") for x in ("S", "T", "Q", "Z"))
+    ref = oracle.greorder(S, T, Q, Z, p.select, w=32, mode=0)
+    assert ref["rc"] == 0
+    rc, bmap = oracle.scan(S)
+    selrow, _ = oracle.select(bmap, p.select)
+    nwin = len(sn.schedule(bmap, selrow, 32)["j1"])
+    L, n = oracle.lib(), S.shape[0]
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)   # noqa: E731
+    for t in range(nwin):
+        sj, s1, s2 = sn.window_swaps(bmap, selrow, 32, t)
+        for j, a1, a2 in zip(sj, s1, s2):
+            assert L.or_gswap(n, ptr(S), n, ptr(T), n, int(j), int(a1), int(a2), ptr(Q), n, n, ptr(Z), n, n) == 0
+    dQ = np.where(np.einsum("ij,ij->j", Q, ref["Q"]) < 0, -1.0, 1.0)
+    dZ = np.where(np.einsum("ij,ij->j", Z, ref["Z"]) < 0, -1.0, 1.0)
+    assert np.abs(S - dQ[:, None] * ref["S"] * dZ[None, :]).max() <= 1e-11 * np.linalg.norm(S)
+    assert np.abs(T - dQ[:, None] * ref["T"] * dZ[None, :]).max() <= 1e-11 * np.linalg.norm(T)
+    assert np.abs(Q - ref["Q"] * dQ).max() <= 1e-11 and np.abs(Z - ref["Z"] * dZ).max() <= 1e-11
