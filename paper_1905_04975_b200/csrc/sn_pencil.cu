@@ -35,7 +35,7 @@ namespace {
 // ---------------------------------------------------------------- the swap transform (device)
 // 4x4 matrices column-major with ld 4 in per-thread arrays.
 
-__host__ __device__ void pl_lartg(double f, double g, double& c, double& s, double& r) {
+__host__ __device__ __forceinline__ void pl_lartg(double f, double g, double& c, double& s, double& r) {
   // c >= 0, r = sign(f) hypot(f, g), [c s; -s c] [f; g] = [r; 0]
   if (g == 0.0) { c = 1.0; s = 0.0; r = f; return; }
   if (f == 0.0) { c = 0.0; s = copysign(1.0, g); r = fabs(g); return; }
@@ -45,62 +45,84 @@ __host__ __device__ void pl_lartg(double f, double g, double& c, double& s, doub
   s = g / r;
 }
 
-__host__ __device__ void pl_eye(double* U, int m) {
+__host__ __device__ __forceinline__ void pl_eye(double* U, int m) {
+#pragma unroll
   for (int i = 0; i < 16; ++i) U[i] = 0.0;
+#pragma unroll
   for (int i = 0; i < m; ++i) U[i * 5] = 1.0;
 }
 
 // C = U^T X V
-__host__ __device__ void pl_congr(const double* U, const double* X, const double* V, double* C, int m) {
+__host__ __device__ __forceinline__ void pl_congr(const double* U, const double* X, const double* V, double* C, int m) {
   double W[16];
+#pragma unroll
   for (int c = 0; c < m; ++c)
+#pragma unroll
     for (int r = 0; r < m; ++r) {
       double acc = 0.0;
+#pragma unroll
       for (int l = 0; l < m; ++l) acc = fma(X[r + 4 * l], V[l + 4 * c], acc);
       W[r + 4 * c] = acc;
     }
+#pragma unroll
   for (int c = 0; c < m; ++c)
+#pragma unroll
     for (int r = 0; r < m; ++r) {
       double acc = 0.0;
+#pragma unroll
       for (int l = 0; l < m; ++l) acc = fma(U[l + 4 * r], W[l + 4 * c], acc);
       C[r + 4 * c] = acc;
     }
 }
 
 // X <- X P
-__host__ __device__ void pl_mulr(double* X, const double* P, int m) {
+__host__ __device__ __forceinline__ void pl_mulr(double* X, const double* P, int m) {
   double W[16];
+#pragma unroll
   for (int c = 0; c < m; ++c)
+#pragma unroll
     for (int r = 0; r < m; ++r) {
       double acc = 0.0;
+#pragma unroll
       for (int l = 0; l < m; ++l) acc = fma(X[r + 4 * l], P[l + 4 * c], acc);
       W[r + 4 * c] = acc;
     }
+#pragma unroll
   for (int i = 0; i < 16; ++i) X[i] = W[i];
 }
 
 // orthogonal H (m x m) whose first p columns span range(M) (M: m x p, destroyed)
-__host__ __device__ void pl_qr_basis(double* M, int m, int p, double* H) {
+__host__ __device__ __forceinline__ void pl_qr_basis(double* M, int m, int p, double* H) {
   pl_eye(H, m);
+#pragma unroll
   for (int c = 0; c < p; ++c) {
     double nrm = 0.0;
+#pragma unroll
     for (int i = c; i < m; ++i) nrm = fma(M[i + 4 * c], M[i + 4 * c], nrm);
     nrm = sqrt(nrm);
     if (nrm == 0.0) continue;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
     for (int i = c; i < m; ++i) v[i] = M[i + 4 * c];
     v[c] += copysign(nrm, M[c + 4 * c]);
     double vtv = 0.0;
+#pragma unroll
     for (int i = c; i < m; ++i) vtv = fma(v[i], v[i], vtv);
     const double f2 = 2.0 / vtv;
+#pragma unroll
     for (int cc = c; cc < p; ++cc) {
       double s = 0.0;
+#pragma unroll
       for (int i = c; i < m; ++i) s = fma(v[i], M[i + 4 * cc], s);
+#pragma unroll
       for (int i = c; i < m; ++i) M[i + 4 * cc] -= (f2 * s) * v[i];
     }
+#pragma unroll
     for (int r = 0; r < m; ++r) {
       double s = 0.0;
+#pragma unroll
       for (int i = c; i < m; ++i) s = fma(H[r + 4 * i], v[i], s);
+#pragma unroll
       for (int i = c; i < m; ++i) H[r + 4 * i] -= (f2 * s) * v[i];
     }
   }
@@ -108,79 +130,114 @@ __host__ __device__ void pl_qr_basis(double* M, int m, int p, double* H) {
 
 // Generalized Sylvester pair S11 R - L S22 = S12, T11 R - L T22 = T12 (G2): Kronecker system
 // x = [vec R; vec L] (column-major vec) by Gaussian elimination with complete pivoting.
-// A = the m x m block of S, B = of T (ld 4).  R, L: n1 x n2 with ld 2.
-__host__ __device__ void pl_gsylv(const double* A, const double* B, int n1, int n2, double* R, double* L) {
-  const int N = n1 * n2, K = 2 * N;
-  double M[8][8], y[8];
-  int cp[8];
-  for (int r = 0; r < 8; ++r)
-    for (int c = 0; c < 8; ++c) M[r][c] = 0.0;
-  for (int jj = 0; jj < n2; ++jj)
-    for (int i = 0; i < n1; ++i) {
-      const int e = i + n1 * jj;
-      for (int l = 0; l < n1; ++l) {
-        M[e][l + n1 * jj] += A[i + 4 * l];
-        M[N + e][l + n1 * jj] += B[i + 4 * l];
+// A = the m x m block of S, B = of T (ld 4).  R, L: n1 x n2 with ld 2.  Compile-time sizes and
+// predicated row / column exchanges keep the system in registers.
+template <int N1, int N2>
+__host__ __device__ __forceinline__ void pl_gsylv(const double* A, const double* B, double* R, double* L) {
+  constexpr int N = N1 * N2, K = 2 * N;
+  double M[K][K], y[K];
+  int cp[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+#pragma unroll
+    for (int c = 0; c < K; ++c) M[r][c] = 0.0;
+#pragma unroll
+  for (int jj = 0; jj < N2; ++jj)
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      const int e = i + N1 * jj;
+#pragma unroll
+      for (int l = 0; l < N1; ++l) {
+        M[e][l + N1 * jj] += A[i + 4 * l];
+        M[N + e][l + N1 * jj] += B[i + 4 * l];
       }
-      for (int l = 0; l < n2; ++l) {
-        M[e][N + i + n1 * l] -= A[(n1 + l) + 4 * (n1 + jj)];
-        M[N + e][N + i + n1 * l] -= B[(n1 + l) + 4 * (n1 + jj)];
+#pragma unroll
+      for (int l = 0; l < N2; ++l) {
+        M[e][N + i + N1 * l] -= A[(N1 + l) + 4 * (N1 + jj)];
+        M[N + e][N + i + N1 * l] -= B[(N1 + l) + 4 * (N1 + jj)];
       }
-      y[e] = A[i + 4 * (n1 + jj)];
-      y[N + e] = B[i + 4 * (n1 + jj)];
+      y[e] = A[i + 4 * (N1 + jj)];
+      y[N + e] = B[i + 4 * (N1 + jj)];
     }
   double mx = 0.0;
+#pragma unroll
   for (int r = 0; r < K; ++r)
+#pragma unroll
     for (int c = 0; c < K; ++c) mx = fmax(mx, fabs(M[r][c]));
   const double smin = fmax(2.220446049250313e-16 * mx, 2.2250738585072014e-308 / 2.220446049250313e-16);
+#pragma unroll
   for (int q = 0; q < K; ++q) cp[q] = q;
+#pragma unroll
   for (int p = 0; p < K; ++p) {
     int pr = p, pc = p;
     double best = -1.0;
+#pragma unroll
     for (int r = p; r < K; ++r)
+#pragma unroll
       for (int c = p; c < K; ++c)
         if (fabs(M[r][c]) > best) { best = fabs(M[r][c]); pr = r; pc = c; }
-    if (pr != p) {
-      for (int c = 0; c < K; ++c) { const double t = M[p][c]; M[p][c] = M[pr][c]; M[pr][c] = t; }
-      const double t = y[p]; y[p] = y[pr]; y[pr] = t;
-    }
-    if (pc != p) {
-      for (int r = 0; r < K; ++r) { const double t = M[r][p]; M[r][p] = M[r][pc]; M[r][pc] = t; }
-      const int t = cp[p]; cp[p] = cp[pc]; cp[pc] = t;
-    }
+#pragma unroll
+    for (int r = p + 1; r < K; ++r)
+      if (r == pr) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) { const double t = M[p][c]; M[p][c] = M[r][c]; M[r][c] = t; }
+        const double t = y[p]; y[p] = y[r]; y[r] = t;
+      }
+#pragma unroll
+    for (int c = p + 1; c < K; ++c)
+      if (c == pc) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) { const double t = M[r][p]; M[r][p] = M[r][c]; M[r][c] = t; }
+        const int t = cp[p]; cp[p] = cp[c]; cp[c] = t;
+      }
     if (fabs(M[p][p]) < smin) M[p][p] = smin;
     const double ip = 1.0 / M[p][p];
+#pragma unroll
     for (int r = p + 1; r < K; ++r) {
       const double f = M[r][p] * ip;
+#pragma unroll
       for (int c = p; c < K; ++c) M[r][c] -= f * M[p][c];
       y[r] -= f * y[p];
     }
   }
-  double x[8], z[8];
+  double z[K], x[K];
+#pragma unroll
   for (int p = K - 1; p >= 0; --p) {
     double acc = y[p];
+#pragma unroll
     for (int c = p + 1; c < K; ++c) acc -= M[p][c] * z[c];
     z[p] = acc / M[p][p];
   }
-  for (int p = 0; p < K; ++p) x[cp[p]] = z[p];
-  for (int jj = 0; jj < n2; ++jj)
-    for (int i = 0; i < n1; ++i) {
-      R[i + 2 * jj] = x[i + n1 * jj];
-      L[i + 2 * jj] = x[N + i + n1 * jj];
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    double v = 0.0;
+#pragma unroll
+    for (int p = 0; p < K; ++p)
+      if (cp[p] == q) v = z[p];
+    x[q] = v;
+  }
+#pragma unroll
+  for (int jj = 0; jj < N2; ++jj)
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      R[i + 2 * jj] = x[i + N1 * jj];
+      L[i + 2 * jj] = x[N + i + N1 * jj];
     }
 }
 
 // Frobenius norm of the n1 x n2 block below the leading n2 x n2 block (G3)
-__host__ __device__ double pl_lowfro(const double* X, int n1, int n2) {
+__host__ __device__ __forceinline__ double pl_lowfro(const double* X, int n1, int n2) {
   double acc = 0.0;
+#pragma unroll
   for (int c = 0; c < n2; ++c)
+#pragma unroll
     for (int r = n2; r < n1 + n2; ++r) acc = fma(X[r + 4 * c], X[r + 4 * c], acc);
   return sqrt(acc);
 }
 
 // 2x2 SVD of a T block (G4): P^T Tb W = diag(s1, s2), s1 >= s2 > 0.  Tb, P, W ld 2.
 // Returns false if Tb is singular.
-__host__ __device__ bool pl_std_t22(const double* Tb, double* P, double* W) {
+__host__ __device__ __forceinline__ bool pl_std_t22(const double* Tb, double* P, double* W) {
   const double a = Tb[0] * Tb[0] + Tb[1] * Tb[1];
   const double b = Tb[2] * Tb[2] + Tb[3] * Tb[3];
   const double g = Tb[0] * Tb[2] + Tb[1] * Tb[3];
@@ -212,11 +269,14 @@ __host__ __device__ bool pl_std_t22(const double* Tb, double* P, double* W) {
 
 // The transform of one swap (G1-G4).  A, B: the m x m blocks of S and T (ld 4, m = n1 + n2).
 // Out: U, V (m x m), An = U^T A V, Bn = U^T B V in standard form.  Returns false = rejected.
-__host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n2, double* U, double* V, double* An,
-                        double* Bn, double* why = nullptr) {
-  const int m = n1 + n2;
+template <int N1, int N2>
+__host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double* B, double* U, double* V, double* An,
+                                                   double* Bn, double* why) {
+  constexpr int n1 = N1, n2 = N2, m = N1 + N2;
   double anorm = 0.0, bnorm = 0.0;   // Frobenius norms of the blocks (G3)
+#pragma unroll
   for (int c = 0; c < m; ++c)
+#pragma unroll
     for (int r = 0; r < m; ++r) {
       anorm = fma(A[r + 4 * c], A[r + 4 * c], anorm);
       bnorm = fma(B[r + 4 * c], B[r + 4 * c], bnorm);
@@ -244,10 +304,13 @@ __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n
   } else {
     // G2
     double R[4] = {0.0, 0.0, 0.0, 0.0}, L[4] = {0.0, 0.0, 0.0, 0.0};
-    pl_gsylv(A, B, n1, n2, R, L);
+    pl_gsylv<N1, N2>(A, B, R, L);
     double Mr[16], Ml[16];
+#pragma unroll
     for (int i = 0; i < 16; ++i) { Mr[i] = 0.0; Ml[i] = 0.0; }
+#pragma unroll
     for (int c = 0; c < n2; ++c) {
+#pragma unroll
       for (int r = 0; r < n1; ++r) { Mr[r + 4 * c] = -R[r + 2 * c]; Ml[r + 4 * c] = -L[r + 2 * c]; }
       Mr[(n1 + c) + 4 * c] = 1.0;
       Ml[(n1 + c) + 4 * c] = 1.0;
@@ -266,22 +329,34 @@ __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n
       pl_congr(I4, B, V, TV, m);
       pl_congr(U, B, I4, UT, m);
       double Ml[16], Mr[16];
+#pragma unroll
       for (int i = 0; i < 16; ++i) { Mr[i] = 0.0; Ml[i] = 0.0; }
+#pragma unroll
       for (int c = 0; c < n2; ++c)
+#pragma unroll
         for (int r = 0; r < m; ++r) Ml[r + 4 * c] = TV[r + 4 * c];
+#pragma unroll
       for (int c = 0; c < n1; ++c)
+#pragma unroll
         for (int r = 0; r < m; ++r) Mr[r + 4 * c] = UT[(n2 + c) + 4 * r];
       pl_qr_basis(Ml, m, n2, Uq);
       pl_qr_basis(Mr, m, n1, H);
+#pragma unroll
       for (int i = 0; i < 16; ++i) Vr[i] = 0.0;
+#pragma unroll
       for (int c = 0; c < n2; ++c)
+#pragma unroll
         for (int r = 0; r < m; ++r) Vr[r + 4 * c] = H[r + 4 * (n1 + c)];
+#pragma unroll
       for (int c = 0; c < n1; ++c)
+#pragma unroll
         for (int r = 0; r < m; ++r) Vr[r + 4 * (n2 + c)] = H[r + 4 * c];
       pl_congr(Uq, A, V, Aq, m);
       pl_congr(U, A, Vr, Ar, m);
       double rq = 0.0, rr = 0.0;
+#pragma unroll
       for (int c = 0; c < n2; ++c)
+#pragma unroll
         for (int r = n2; r < m; ++r) { rq = fma(Aq[r + 4 * c], Aq[r + 4 * c], rq); rr = fma(Ar[r + 4 * c], Ar[r + 4 * c], rr); }
       if (rq <= rr) { for (int i = 0; i < 16; ++i) U[i] = Uq[i]; }
       else { for (int i = 0; i < 16; ++i) V[i] = Vr[i]; }
@@ -290,7 +365,9 @@ __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n
   }
   // G3
   double resA = 0.0, resB = 0.0;
+#pragma unroll
   for (int c = 0; c < n2; ++c)
+#pragma unroll
     for (int r = n2; r < m; ++r) {
       resA = fma(An[r + 4 * c], An[r + 4 * c], resA);
       resB = fma(Bn[r + 4 * c], Bn[r + 4 * c], resB);
@@ -299,9 +376,12 @@ __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n
     if (why) { why[0] = 1.0; why[1] = fmax(sqrt(resA) / thA, sqrt(resB) / thB); }
     return false;
   }
+#pragma unroll
   for (int c = 0; c < n2; ++c)
+#pragma unroll
     for (int r = n2; r < m; ++r) { An[r + 4 * c] = 0.0; Bn[r + 4 * c] = 0.0; }
   // G4: 2x2 blocks
+#pragma unroll
   for (int q = 0; q < 2; ++q) {
     int p = -1;
     if (q == 0 && n2 == 2) p = 0;
@@ -321,6 +401,7 @@ __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n
     double A2[16], B2[16];
     pl_congr(Pm, An, Wm, A2, m);
     pl_congr(Pm, Bn, Wm, B2, m);
+#pragma unroll
     for (int i = 0; i < 16; ++i) { An[i] = A2[i]; Bn[i] = B2[i]; }
     Bn[(p + 1) + 4 * p] = 0.0;
     Bn[p + 4 * (p + 1)] = 0.0;
@@ -336,15 +417,48 @@ __host__ __device__ bool pl_swap(const double* A, const double* B, int n1, int n
     }
   }
   // G4: moved 1x1 blocks with t >= 0
+#pragma unroll
   for (int q = 0; q < 2; ++q) {
     int p = -1;
     if (q == 0 && n2 == 1) p = 0;
     if (q == 1 && n1 == 1) p = n2;
     if (p < 0 || !(Bn[p + 4 * p] < 0.0)) continue;
+#pragma unroll
     for (int c = 0; c < m; ++c) { An[p + 4 * c] = -An[p + 4 * c]; Bn[p + 4 * c] = -Bn[p + 4 * c]; }
+#pragma unroll
     for (int r = 0; r < m; ++r) U[r + 4 * p] = -U[r + 4 * p];
   }
   return true;
+}
+
+__host__ __device__ inline bool pl_swap(const double* A, const double* B, int n1, int n2, double* U, double* V,
+                                        double* An, double* Bn, double* why = nullptr) {
+  if (n1 == 1 && n2 == 1) return pl_swap_t<1, 1>(A, B, U, V, An, Bn, why);
+  if (n1 == 1) return pl_swap_t<1, 2>(A, B, U, V, An, Bn, why);
+  if (n2 == 1) return pl_swap_t<2, 1>(A, B, U, V, An, Bn, why);
+  return pl_swap_t<2, 2>(A, B, U, V, An, Bn, why);
+}
+
+// One thread's transform of a swap of type (N1, N2) at window row j into the record R.
+template <int N1, int N2>
+__device__ __forceinline__ bool pl_transform(const double* Sw, int64_t ldS, const double* Tw, int64_t ldT, int j,
+                                             double* R, double* why) {
+  constexpr int m = N1 + N2;
+  double A[16], B[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { A[i] = 0.0; B[i] = 0.0; }
+#pragma unroll
+  for (int c = 0; c < m; ++c)
+#pragma unroll
+    for (int r = 0; r < m; ++r) {
+      A[r + 4 * c] = Sw[(j + r) + (int64_t)(j + c) * ldS];
+      B[r + 4 * c] = Tw[(j + r) + (int64_t)(j + c) * ldT];
+    }
+  double U[16], V[16], An[16], Bn[16];
+  const bool ok = pl_swap_t<N1, N2>(A, B, U, V, An, Bn, why);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { R[i] = U[i]; R[16 + i] = V[i]; R[32 + i] = An[i]; R[48 + i] = Bn[i]; }
+  return ok;
 }
 
 // ---------------------------------------------------------------- the window task (device)
@@ -426,17 +540,14 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     // (1) transforms, one thread per swap
     if (tid < cnt) {
       const int64_t s = s0 + b0 + tid;
-      const int j = a.sj[s], n1 = a.s12[s] >> 4, n2 = a.s12[s] & 15, m = n1 + n2;
-      double A[16], B[16];
-      for (int i = 0; i < 16; ++i) { A[i] = 0.0; B[i] = 0.0; }
-      for (int c = 0; c < m; ++c)
-        for (int r = 0; r < m; ++r) {
-          A[r + 4 * c] = Sw[(j + r) + (int64_t)(j + c) * ldS];
-          B[r + 4 * c] = Tw[(j + r) + (int64_t)(j + c) * ldT];
-        }
+      const int j = a.sj[s], n1 = a.s12[s] >> 4, n2 = a.s12[s] & 15;
       double* R = rec + tid * kRecD;
       double why[2] = {0.0, 0.0};
-      bool ok = pl_swap(A, B, n1, n2, R, R + 16, R + 32, R + 48, why);
+      bool ok;
+      if (n1 == 1 && n2 == 1) ok = pl_transform<1, 1>(Sw, ldS, Tw, ldT, j, R, why);
+      else if (n1 == 1) ok = pl_transform<1, 2>(Sw, ldS, Tw, ldT, j, R, why);
+      else if (n2 == 1) ok = pl_transform<2, 1>(Sw, ldS, Tw, ldT, j, R, why);
+      else ok = pl_transform<2, 2>(Sw, ldS, Tw, ldT, j, R, why);
       if (wd.order == a.force_order && a.sidx[s] == a.force_swap) { ok = false; why[0] = 0.0; }
       if (!ok) {
         const int key = a.sidx[s];
