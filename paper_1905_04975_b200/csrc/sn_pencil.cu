@@ -88,7 +88,9 @@ __host__ __device__ __forceinline__ void pl_mulr(double* X, const double* P, int
       W[r + 4 * c] = acc;
     }
 #pragma unroll
-  for (int i = 0; i < 16; ++i) X[i] = W[i];
+  for (int c = 0; c < m; ++c)
+#pragma unroll
+    for (int r = 0; r < m; ++r) X[r + 4 * c] = W[r + 4 * c];   // entries outside m x m stay 0
 }
 
 // orthogonal H (m x m) whose first p columns span range(M) (M: m x p, destroyed)
@@ -591,13 +593,18 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       const int64_t ld = isT ? ldT : ldS;
       const int64_t c = j + m + (isT ? e - nl : e);
       double x[4], y[4];
-      for (int t = 0; t < m; ++t) x[t] = X[(j + t) + c * ld];
-      for (int t = 0; t < m; ++t) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) x[t] = t < m ? X[(j + t) + c * ld] : 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
         double acc = 0.0;
-        for (int l = 0; l < m; ++l) acc = fma(R[l + 4 * t], x[l], acc);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc = fma(R[l + 4 * t], x[l], acc);   // U is zero-padded
         y[t] = acc;
       }
-      for (int t = 0; t < m; ++t) X[(j + t) + c * ld] = y[t];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t < m) X[(j + t) + c * ld] = y[t];
     }
     __syncthreads();
     if (tid == 0) {
@@ -627,13 +634,18 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
         X = isV ? VR : UL; ld = kZld; r = isV ? e3 - k : e3; F = isV ? R + 16 : R;
       }
       double x[4], y[4];
-      for (int t = 0; t < m; ++t) x[t] = X[r + (int64_t)(j + t) * ld];
-      for (int t = 0; t < m; ++t) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) x[t] = t < m ? X[r + (int64_t)(j + t) * ld] : 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
         double acc = 0.0;
-        for (int l = 0; l < m; ++l) acc = fma(x[l], F[l + 4 * t], acc);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc = fma(x[l], F[l + 4 * t], acc);   // V is zero-padded
         y[t] = acc;
       }
-      for (int t = 0; t < m; ++t) X[r + (int64_t)(j + t) * ld] = y[t];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t < m) X[r + (int64_t)(j + t) * ld] = y[t];
     }
     done_steps = st + 1;
     __syncthreads();
