@@ -63,11 +63,15 @@ for q in range(len(sj)):
 order = sorted(range(len(sj)), key=lambda q: (steps[q], q))
 L = oracle.lib()
 ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+lapack_rejects = 0
 for q in order:
     j = int(sj[q]) - j1
     n1, n2 = int(s1[q]), int(s2[q])
     m = n1 + n2
     A0, B0 = D[j:j + m, j:j + m].copy(order="F"), E[j:j + m, j:j + m].copy(order="F")
+    if m == 4:
+        info4 = lapack.dtgexc(A0.copy(), B0.copy(), np.eye(m), np.eye(m), n1 + 1, 1)[5]
+        lapack_rejects += int(info4 != 0)
     if L.or_gswap(k, ptr(D), k, ptr(E), k, j, n1, n2, None, 0, 0, None, 0, 0):
         a, b, _, _, _, info = lapack.dtgexc(A0.copy(), B0.copy(), np.eye(m), np.eye(m), n1 + 1, 1)
         print(json.dumps({"window": T, "list_index": q, "row": j1 + j, "n1": n1, "n2": n2, "lapack_info": int(info),
@@ -75,3 +79,4 @@ for q in order:
         break
 else:
     print("no rejection in the oracle replay of window", T)
+print("2x2|2x2 swaps of the window that LAPACK dtgexc rejects on the same blocks:", lapack_rejects)
