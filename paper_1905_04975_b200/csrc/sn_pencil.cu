@@ -519,6 +519,8 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   const int64_t ldS = a.ldS, ldT = a.ldT;
   __shared__ int16_t zlo[kZld], zhi[kZld];
   __shared__ int s_pre[kZld + 1];
+  __shared__ int16_t s_j[kZld];      // per swap of the current step: window row, size m
+  __shared__ int8_t s_m[kZld];
   __shared__ int s_rej;
   __shared__ double s_why[2];
   for (int64_t i = tid; i < kZslot; i += blockDim.x) {
@@ -543,6 +545,8 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     if (tid < cnt) {
       const int64_t s = s0 + b0 + tid;
       const int j = a.sj[s], n1 = a.s12[s] >> 4, n2 = a.s12[s] & 15;
+      s_j[tid] = (int16_t)j;
+      s_m[tid] = (int8_t)(n1 + n2);
       double* R = rec + tid * kRecD;
       double why[2] = {0.0, 0.0};
       bool ok;
@@ -560,8 +564,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     if (s_rej != 0x7fffffff) break;
     // (2) column intervals of the accumulators; row-application task counts
     if (tid < cnt) {
-      const int64_t s = s0 + b0 + tid;
-      const int j = a.sj[s], m = (a.s12[s] >> 4) + (a.s12[s] & 15);
+      const int j = s_j[tid], m = s_m[tid];
       int lo = zlo[j], hi = zhi[j];
       for (int c = 1; c < m; ++c) { lo = min(lo, (int)zlo[j + c]); hi = max(hi, (int)zhi[j + c]); }
       for (int c = 0; c < m; ++c) { zlo[j + c] = (int16_t)lo; zhi[j + c] = (int16_t)hi; }
@@ -569,8 +572,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     if (tid == 0) {
       s_pre[0] = 0;
       for (int i = 0; i < cnt; ++i) {
-        const int64_t s = s0 + b0 + i;
-        const int j = a.sj[s], m = (a.s12[s] >> 4) + (a.s12[s] & 15);
+        const int j = s_j[i], m = s_m[i];
         s_pre[i + 1] = s_pre[i] + 2 * (k - j - m) + m * m;
       }
     }
@@ -578,8 +580,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     // (3) rows j..j+m-1 right of each block (S, T) and the new diagonal blocks
     for (int q = tid; q < s_pre[cnt]; q += blockDim.x) {
       const int i = pl_find(s_pre, cnt, q);
-      const int64_t s = s0 + b0 + i;
-      const int j = a.sj[s], m = (a.s12[s] >> 4) + (a.s12[s] & 15);
+      const int j = s_j[i], m = s_m[i];
       const double* R = rec + i * kRecD;
       const int nl = k - j - m, e = q - s_pre[i];
       if (e >= 2 * nl) {
@@ -608,18 +609,13 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     }
     __syncthreads();
     if (tid == 0) {
-      for (int i = 0; i < cnt; ++i) {
-        const int64_t s = s0 + b0 + i;
-        const int j = a.sj[s];
-        s_pre[i + 1] = s_pre[i] + 2 * j + 2 * k;
-      }
+      for (int i = 0; i < cnt; ++i) s_pre[i + 1] = s_pre[i] + 2 * s_j[i] + 2 * k;
     }
     __syncthreads();
     // (4) columns j..j+m-1 above each block (S, T) and of UL, VR
     for (int q = tid; q < s_pre[cnt]; q += blockDim.x) {
       const int i = pl_find(s_pre, cnt, q);
-      const int64_t s = s0 + b0 + i;
-      const int j = a.sj[s], m = (a.s12[s] >> 4) + (a.s12[s] & 15);
+      const int j = s_j[i], m = s_m[i];
       const double* R = rec + i * kRecD;
       const int e = q - s_pre[i];
       double* X;
