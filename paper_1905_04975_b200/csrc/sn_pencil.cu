@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   __shared__ int s_pre[kZld + 1];
   __shared__ int16_t s_j[kZld];      // per swap of the current step: window row, size m
   __shared__ int8_t s_m[kZld];
+  __shared__ int16_t s_lo[kZld], s_hi[kZld];   // merged nonzero row interval of its UL/VR columns
   __shared__ int s_rej;
   __shared__ double s_why[2];
   for (int64_t i = tid; i < kZslot; i += blockDim.x) {
@@ -568,6 +569,8 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       int lo = zlo[j], hi = zhi[j];
       for (int c = 1; c < m; ++c) { lo = min(lo, (int)zlo[j + c]); hi = max(hi, (int)zhi[j + c]); }
       for (int c = 0; c < m; ++c) { zlo[j + c] = (int16_t)lo; zhi[j + c] = (int16_t)hi; }
+      s_lo[tid] = (int16_t)lo;
+      s_hi[tid] = (int16_t)hi;
     }
     if (tid == 0) {
       s_pre[0] = 0;
@@ -609,7 +612,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     }
     __syncthreads();
     if (tid == 0) {
-      for (int i = 0; i < cnt; ++i) s_pre[i + 1] = s_pre[i] + 2 * s_j[i] + 2 * k;
+      for (int i = 0; i < cnt; ++i) s_pre[i + 1] = s_pre[i] + 2 * s_j[i] + 2 * (s_hi[i] - s_lo[i] + 1);
     }
     __syncthreads();
     // (4) columns j..j+m-1 above each block (S, T) and of UL, VR
@@ -625,9 +628,10 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
         const bool isT = e >= j;
         X = isT ? Tw : Sw; ld = isT ? ldT : ldS; r = isT ? e - j : e; F = R + 16;
       } else {
-        const int e3 = e - 2 * j;
-        const bool isV = e3 >= k;
-        X = isV ? VR : UL; ld = kZld; r = isV ? e3 - k : e3; F = isV ? R + 16 : R;
+        // UL / VR columns j..j+m-1 are exact zeros outside the merged interval [lo, hi]
+        const int e3 = e - 2 * j, len = s_hi[i] - s_lo[i] + 1;
+        const bool isV = e3 >= len;
+        X = isV ? VR : UL; ld = kZld; r = s_lo[i] + (isV ? e3 - len : e3); F = isV ? R + 16 : R;
       }
       double x[4], y[4];
 #pragma unroll
