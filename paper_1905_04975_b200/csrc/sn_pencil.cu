@@ -576,76 +576,92 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       s_pre[0] = 0;
       for (int i = 0; i < cnt; ++i) {
         const int j = s_j[i], m = s_m[i];
-        s_pre[i + 1] = s_pre[i] + 2 * (k - j - m) + m * m;
+        s_pre[i + 1] = s_pre[i] + 2 * (k - j - m);
       }
     }
     __syncthreads();
-    // (3) rows j..j+m-1 right of each block (S, T) and the new diagonal blocks
-    for (int q = tid; q < s_pre[cnt]; q += blockDim.x) {
-      const int i = pl_find(s_pre, cnt, q);
-      const int j = s_j[i], m = s_m[i];
+    // (3) rows j..j+m-1 right of each block (S, T); the new diagonal blocks
+    for (int q = tid; q < cnt * 16; q += blockDim.x) {
+      const int i = q >> 4, d = q & 15, m = s_m[i];
+      if (d >= m * m) continue;
+      const int j = s_j[i], r = d % m, c = d / m;
       const double* R = rec + i * kRecD;
-      const int nl = k - j - m, e = q - s_pre[i];
-      if (e >= 2 * nl) {
-        const int d = e - 2 * nl, r = d % m, c = d / m;
-        Sw[(j + r) + (int64_t)(j + c) * ldS] = R[32 + r + 4 * c];
-        Tw[(j + r) + (int64_t)(j + c) * ldT] = R[48 + r + 4 * c];
-        continue;
-      }
-      const bool isT = e >= nl;
-      double* X = isT ? Tw : Sw;
-      const int64_t ld = isT ? ldT : ldS;
-      const int64_t c = j + m + (isT ? e - nl : e);
-      double x[4], y[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) x[t] = t < m ? X[(j + t) + c * ld] : 0.0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < 4; ++l) acc = fma(R[l + 4 * t], x[l], acc);   // U is zero-padded
-        y[t] = acc;
-      }
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (t < m) X[(j + t) + c * ld] = y[t];
+      Sw[(j + r) + (int64_t)(j + c) * ldS] = R[32 + r + 4 * c];
+      Tw[(j + r) + (int64_t)(j + c) * ldT] = R[48 + r + 4 * c];
     }
-    __syncthreads();
-    if (tid == 0) {
-      for (int i = 0; i < cnt; ++i) s_pre[i + 1] = s_pre[i] + 2 * s_j[i] + 2 * (s_hi[i] - s_lo[i] + 1);
-    }
-    __syncthreads();
-    // (4) columns j..j+m-1 above each block (S, T) and of UL, VR
-    for (int q = tid; q < s_pre[cnt]; q += blockDim.x) {
+    // a task = one m-vector of S, T, UL or VR times an m x m factor G: y[t] = sum_l G[l + 4t] x[l]
+    // (rows: x along a column, G = U; columns: x along a row, G = V or U); two tasks per
+    // thread and round, loads first, so their memory latencies overlap (tasks are disjoint)
+    auto row_task = [&](int q, double*& X, int64_t& base, int64_t& stride, const double*& G, int& m) {
       const int i = pl_find(s_pre, cnt, q);
-      const int j = s_j[i], m = s_m[i];
+      const int j = s_j[i];
+      m = s_m[i];
+      G = rec + i * kRecD;
+      const int nl = k - j - m, e = q - s_pre[i];
+      const bool isT = e >= nl;
+      X = isT ? Tw : Sw;
+      const int64_t ld = isT ? ldT : ldS;
+      base = j + (int64_t)(j + m + (isT ? e - nl : e)) * ld;
+      stride = 1;
+    };
+    auto col_task = [&](int q, double*& X, int64_t& base, int64_t& stride, const double*& G, int& m) {
+      const int i = pl_find(s_pre, cnt, q);
+      const int j = s_j[i];
+      m = s_m[i];
       const double* R = rec + i * kRecD;
       const int e = q - s_pre[i];
-      double* X;
-      int64_t ld, r;
-      const double* F;
+      int64_t r;
       if (e < 2 * j) {
         const bool isT = e >= j;
-        X = isT ? Tw : Sw; ld = isT ? ldT : ldS; r = isT ? e - j : e; F = R + 16;
+        X = isT ? Tw : Sw; stride = isT ? ldT : ldS; r = isT ? e - j : e; G = R + 16;
       } else {
         // UL / VR columns j..j+m-1 are exact zeros outside the merged interval [lo, hi]
         const int e3 = e - 2 * j, len = s_hi[i] - s_lo[i] + 1;
         const bool isV = e3 >= len;
-        X = isV ? VR : UL; ld = kZld; r = s_lo[i] + (isV ? e3 - len : e3); F = isV ? R + 16 : R;
+        X = isV ? VR : UL; stride = kZld; r = s_lo[i] + (isV ? e3 - len : e3); G = isV ? R + 16 : R;
       }
-      double x[4], y[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) x[t] = t < m ? X[r + (int64_t)(j + t) * ld] : 0.0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < 4; ++l) acc = fma(x[l], F[l + 4 * t], acc);   // V is zero-padded
-        y[t] = acc;
+      base = r + (int64_t)j * stride;
+    };
+    for (int phase = 0; phase < 2; ++phase) {
+      if (phase == 1) {
+        __syncthreads();
+        if (tid == 0)
+          for (int i = 0; i < cnt; ++i) s_pre[i + 1] = s_pre[i] + 2 * s_j[i] + 2 * (s_hi[i] - s_lo[i] + 1);
+        __syncthreads();
       }
+      const int total = s_pre[cnt];
+      for (int q0 = tid; q0 < total; q0 += 2 * blockDim.x) {
+        double* X[2];
+        int64_t base[2], stride[2];
+        const double* G[2];
+        int m[2];
+        double x[2][4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (t < m) X[r + (int64_t)(j + t) * ld] = y[t];
+        for (int u = 0; u < 2; ++u) {
+          const int q = q0 + u * blockDim.x;
+          m[u] = 0;
+          if (q < total) {
+            if (phase == 0) row_task(q, X[u], base[u], stride[u], G[u], m[u]);
+            else col_task(q, X[u], base[u], stride[u], G[u], m[u]);
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t) x[u][t] = t < m[u] ? X[u][base[u] + t * stride[u]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          double y[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            double acc = 0.0;
+#pragma unroll
+            for (int l = 0; l < 4; ++l) acc = (l < m[u]) ? fma(G[u][l + 4 * t], x[u][l], acc) : acc;
+            y[t] = acc;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (t < m[u]) X[u][base[u] + t * stride[u]] = y[t];
+        }
+      }
     }
     done_steps = st + 1;
     __syncthreads();
