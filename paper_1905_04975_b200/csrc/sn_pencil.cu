@@ -791,10 +791,14 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
       }
       hstep_base.push_back((int64_t)hstep.size());
       for (int32_t t = 0; t <= ns; ++t) hstep.push_back(per[t]);
+      // within a step, group the swaps by type (consecutive threads, so most warps run one
+      // specialisation of the transform), in list order within a type
       std::vector<int64_t> ord((size_t)cnt);
       {
-        std::vector<int32_t> fill(per.begin(), per.end() - 1);
-        for (int64_t q = 0; q < cnt; ++q) ord[fill[stp[q]]++] = q;   // stable within a step
+        std::vector<int32_t> fill((size_t)ns * 4 + 1, 0);   // counting sort by (step, type)
+        for (int64_t q = 0; q < cnt; ++q) fill[(size_t)stp[q] * 4 + (a1[q] - 1) * 2 + (a2[q] - 1) + 1]++;
+        for (size_t t = 1; t < fill.size(); ++t) fill[t] += fill[t - 1];
+        for (int64_t q = 0; q < cnt; ++q) ord[fill[(size_t)stp[q] * 4 + (a1[q] - 1) * 2 + (a2[q] - 1)]++] = q;
       }
       for (int64_t q = 0; q < cnt; ++q) {
         const int64_t o = ord[q];
