@@ -118,8 +118,7 @@ def workload_desc(cfg, prob):
 
 def oracle_sample(prob, target_gflop, device_S0, device_Q0):
     """Time the CPU oracle (mode ii, 1 core) on the first K windows of the workload."""
-    import oracle
-    import paper_1905_04975_b200 as sn   # sizing of the sample only (host schedule)
+    import oracle   # the reference arm touches only oracle/ (sample sizing included)
     S = np.asfortranarray(device_S0.cpu().numpy().T)
     Q = np.asfortranarray(device_Q0.cpu().numpy().T)
     sub = np.diag(S, -1) != 0.0
@@ -137,8 +136,8 @@ def oracle_sample(prob, target_gflop, device_S0, device_Q0):
         s = 2 if bm[i] == 1 else 1
         sel8[i:i + s] = 1 if prob.select[i:i + s].any() else 0
         i += s
-    sch = sn.schedule(bm, sel8, prob.w)
-    k, j1 = sch["k"].astype(float), sch["j1"].astype(float)
+    sch = oracle.schedule(bm, sel8, prob.w)
+    k, j1 = (sch["j2"] - sch["j1"]).astype(float), sch["j1"].astype(float)
     fl = 2 * k * k * ((prob.n - j1 - k) + j1 + prob.n)
     K = int(max(1, np.searchsorted(np.cumsum(fl), target_gflop * 1e9)))
     t0 = time.perf_counter()

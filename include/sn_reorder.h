@@ -54,7 +54,9 @@ typedef struct sn_opts {
                                 SURVEY §8c-2: ks = w/2 rows of movers per chain group. */
   int64_t inner_window;      /* rows of the in-kernel inner windows (default 64, <= 64) */
   int64_t max_windows;       /* stop after this many windows (prefix runs); < 0 = all */
-  int64_t force_reject_window; /* debug: window (schedule order) whose swap is rejected */
+  int64_t force_reject_window; /* debug: window (schedule order) whose swap is rejected; a value
+                                  <= -2 rejects in every window of DAG level -2 - value (several
+                                  partial windows in one level); -1 none */
   int64_t force_reject_swap;   /* debug: swap index (execution order within that window) */
   int32_t validate_lower;    /* 1: also check that S is exactly 0 below the subdiagonal
                                 (n^2/2 device reads); the subdiagonal is always checked */

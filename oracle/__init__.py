@@ -55,6 +55,7 @@ def lib():
         _lib.or_sylv.restype = i32
         _lib.or_swap.argtypes = [i64, p, i64, i64, i32, i32, p, i64, i64]
         _lib.or_swap.restype = i32
+        _lib.or_swap_last_reject.restype = i32
         _lib.or_scan.argtypes = [i64, p, i64, p]
         _lib.or_scan.restype = i32
         _lib.or_select.argtypes = [i64, p, p, p, C.POINTER(C.c_int64)]
@@ -64,10 +65,18 @@ def lib():
         _lib.or_reorder.argtypes = [i32, i64, p, i64, p, i64, p, C.POINTER(C.c_int64), i64, i64, i64,
                                     p, C.POINTER(Stats)]
         _lib.or_reorder.restype = i32
+        _lib.or_reorder_q.argtypes = [i32, i64, p, i64, p, i64, i64, p, C.POINTER(C.c_int64), i64, i64, i64,
+                                      p, C.POINTER(Stats)]
+        _lib.or_reorder_q.restype = i32
         _lib.or_gsylv.argtypes = [i32, i32, p, p, p, p, p, p, p, p]
         _lib.or_gsylv.restype = i32
         _lib.or_gswap.argtypes = [i64, p, i64, p, i64, i64, i32, i32, p, i64, i64, p, i64, i64]
         _lib.or_gswap.restype = i32
+        _lib.or_gswap_last_variant.restype = i32
+        _lib.or_eig_count.argtypes = [i64, p, i64, p, C.POINTER(C.c_int64)]
+        _lib.or_eig_count.restype = i32
+        _lib.or_eigvec.argtypes = [i64, p, i64, p, i64, p, p, i64, p]
+        _lib.or_eigvec.restype = i32
         _lib.or_greorder.argtypes = [i32, i64, p, i64, p, i64, p, i64, p, i64, p, C.POINTER(C.c_int64),
                                      i64, i64, i64, p, C.POINTER(Stats)]
         _lib.or_greorder.restype = i32
@@ -162,12 +171,18 @@ def schedule(bmap, selrow, w: int):
     return {"j1": j1, "j2": j2, "off": off, "swap_j": sj, "swap_n1": s1, "swap_n2": s2}
 
 
+def swap_last_reject() -> int:
+    """Why the last swap() rejected: 0 accepted, 1 weak stability test, 2 2x2 split (R6)."""
+    return lib().or_swap_last_reject()
+
+
 def reorder(S, Q, select_rows, w: int, mode: int = 1, max_windows: int = -1,
             force_reject_at: int = -1, inplace: bool = False):
     """Reorder (Eq. (7)).  mode 1 = accumulated-naive (Fig. 1b), 0 = unblocked (Fig. 1a).
 
     Returns dict(rc, S, Q, select, m, bmap, stats).  S, Q are Fortran fp64 arrays
-    (copied unless inplace=True and already Fortran fp64)."""
+    (copied unless inplace=True and already Fortran fp64).  Q may hold a sample of nq <= n
+    rows (shape (nq, n)): those rows of the full result (or_reorder_q)."""
     if inplace:
         assert S.dtype == np.float64 and S.flags.f_contiguous
         Sx = S
@@ -180,8 +195,10 @@ def reorder(S, Q, select_rows, w: int, mode: int = 1, max_windows: int = -1,
     m = C.c_int64()
     bmap = np.zeros(n, np.int8)
     st = Stats()
-    rc = lib().or_reorder(mode, n, _ptr(Sx), max(n, 1), _ptr(Qx), max(n, 1), _ptr(sel), C.byref(m), w,
-                          max_windows, force_reject_at, _ptr(bmap), C.byref(st))
+    nq = n if Qx is None else Qx.shape[0]
+    assert Qx is None or Qx.shape[1] == n
+    rc = lib().or_reorder_q(mode, n, _ptr(Sx), max(n, 1), _ptr(Qx), max(nq, 1), nq, _ptr(sel), C.byref(m), w,
+                            max_windows, force_reject_at, _ptr(bmap), C.byref(st))
     stats = {f: getattr(st, f) for f, _ in Stats._fields_}
     stats["swaps_by_type"] = list(st.swaps_by_type)
     return {"rc": rc, "S": Sx, "Q": Qx, "select": sel, "m": m.value, "bmap": bmap, "stats": stats}
@@ -218,6 +235,12 @@ def gswap(S, T, j: int, n1: int, n2: int, Ql=None, Zr=None):
     return rc, S, T, Qc, Zc
 
 
+def gswap_last_variant() -> int:
+    """Which branch the last gswap() took: 0 G1, 1 left / 2 right re-triangularisation
+    kept (G2), -1 rejected."""
+    return lib().or_gswap_last_variant()
+
+
 def greorder(S, T, Q, Z, select_rows, w: int, mode: int = 1, max_windows: int = -1,
              force_reject_at: int = -1):
     """Generalized reordering (Eq. (7) right form).  Returns dict(rc, S, T, Q, Z, select, m,
@@ -237,3 +260,24 @@ def greorder(S, T, Q, Z, select_rows, w: int, mode: int = 1, max_windows: int = 
     stats["swaps_by_type"] = list(st.swaps_by_type)
     return {"rc": rc, "S": Sx, "T": Tx, "Q": Qx, "Z": Zx, "select": sel, "m": m.value, "bmap": bmap,
             "stats": stats}
+
+
+# ---- eigenvectors (sn_oracle.h) ----------------------------------------
+
+def eigvec(S, Q, select_rows):
+    """Right eigenvectors of the selected blocks of the quasi-triangular S (Eq. (5)),
+    back-transformed by Q (Eq. (6)) if given, normalised as LAPACK xTREVC.  Returns
+    (rc, X (n x ncols, Fortran), scale_exp (per column))."""
+    Sx = _f64(S)
+    Sx = Sx if Sx.flags.f_contiguous else Sx.copy(order="F")
+    n = Sx.shape[0]
+    sel = np.ascontiguousarray(select_rows, np.int32)
+    nc = C.c_int64()
+    rc = lib().or_eig_count(n, _ptr(Sx), max(n, 1), _ptr(sel), C.byref(nc))
+    if rc:
+        return rc, None, None
+    Qx = None if Q is None else (_f64(Q) if _f64(Q).flags.f_contiguous else _f64(Q).copy(order="F"))
+    X = np.zeros((n, nc.value), order="F")
+    e = np.zeros(max(nc.value, 1), np.int32)
+    rc = lib().or_eigvec(n, _ptr(Sx), max(n, 1), _ptr(Qx), max(n, 1), _ptr(sel), _ptr(X), max(n, 1), _ptr(e))
+    return rc, X, e[:nc.value]

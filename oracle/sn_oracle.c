@@ -44,6 +44,9 @@ static double lapy2(double x, double y) {
  * Givens rotation, SURVEY c4 #2 (LAPACK >= 3.10 xLARTG): c >= 0,
  * r = sign(f) * hypot(f, g), s = g / r.  g == 0 -> identity; f == 0 ->
  * (c, s) = (0, sign(g)).
+ * Attribution: follows the algorithm and safe-scaling constants of the reference
+ * LAPACK routine named above (LAPACK, Univ. of Tennessee / UC Berkeley / Univ. of
+ * Colorado Denver / NAG Ltd., modified-BSD licence), restated in C here.
  * ------------------------------------------------------------------------- */
 void or_lartg(double f, double g, double* c, double* s, double* r) {
   const double safmin = DBL_MIN, safmax = 1.0 / DBL_MIN;
@@ -73,6 +76,9 @@ void or_lartg(double f, double g, double* c, double* s, double* r) {
  * 3-element Householder reflector, SURVEY c4 #3 (LAPACK xLARFG convention):
  * beta = -sign(alpha) * ||(alpha, x)||, tau = (beta - alpha) / beta,
  * v = (1, x / (alpha - beta)).  tau = 0 (H = I) when x == 0.
+ * Attribution: follows the algorithm and safe-scaling constants of the reference
+ * LAPACK routine named above (LAPACK, Univ. of Tennessee / UC Berkeley / Univ. of
+ * Colorado Denver / NAG Ltd., modified-BSD licence), restated in C here.
  * ------------------------------------------------------------------------- */
 void or_larfg3(double* alpha, double x[2], double* tau) {
   const double safmin = DBL_MIN / (DBL_EPSILON * 0.5); /* dlamch('S')/dlamch('E') */
@@ -99,6 +105,9 @@ void or_larfg3(double* alpha, double x[2], double* tau) {
 
 /* ---------------------------------------------------------------------------
  * Standardisation of a 2x2 block, SURVEY c4 #6 (xLANV2 semantics).
+ * Attribution: follows the algorithm and safe-scaling constants of the reference
+ * LAPACK routine named above (LAPACK, Univ. of Tennessee / UC Berkeley / Univ. of
+ * Colorado Denver / NAG Ltd., modified-BSD licence), restated in C here.
  * ------------------------------------------------------------------------- */
 void or_lanv2(double* pa, double* pb, double* pc, double* pd, double* pcs, double* psn) {
   const double eps = DBL_EPSILON;          /* dlamch('P') */
@@ -323,9 +332,13 @@ static void rot_right(double* A, int64_t lda, int64_t c0, int64_t r0, int64_t r1
 /* ---------------------------------------------------------------------------
  * Adjacent block swap.
  * ------------------------------------------------------------------------- */
+static int g_last_reject = 0;   /* diagnostics: why the last or_swap call rejected */
+int or_swap_last_reject(void) { return g_last_reject; }
+
 int or_swap(int64_t nt, double* T, int64_t ldt, int64_t j, int n1, int n2,
             double* Qm, int64_t ldq, int64_t nq) {
   const int nd = n1 + n2;
+  g_last_reject = 0;
   if (n1 == 1 && n2 == 1) {
     /* Givens rotation from (t12, t22 - t11); the diagonal entries are swapped
      * exactly and t12 is left untouched. */
@@ -412,7 +425,7 @@ int or_swap(int64_t nt, double* T, int64_t ldt, int64_t j, int n1, int n2,
     resid = dmax(dmax(fabs(Dn[2 + 4 * 0]), fabs(Dn[2 + 4 * 1])),
                  dmax(fabs(Dn[3 + 4 * 0]), fabs(Dn[3 + 4 * 1])));
   }
-  if (!(resid <= thresh)) return 1;
+  if (!(resid <= thresh)) { g_last_reject = 1; return 1; }
 
   /* exact zeros below the new blocks and the exact moved 1x1 eigenvalue (c4 #7) */
   if (n1 == 1) {
@@ -435,7 +448,7 @@ int or_swap(int64_t nt, double* T, int64_t ldt, int64_t j, int n1, int n2,
     double a = Dn[p + 4 * p], b = Dn[p + 4 * (p + 1)], c = Dn[(p + 1) + 4 * p], d = Dn[(p + 1) + 4 * (p + 1)];
     double cs, sn;
     or_lanv2(&a, &b, &c, &d, &cs, &sn);
-    if (c == 0.0) return 1;
+    if (c == 0.0) { g_last_reject = 2; return 1; }
     Dn[p + 4 * p] = a; Dn[p + 4 * (p + 1)] = b; Dn[(p + 1) + 4 * p] = c; Dn[(p + 1) + 4 * (p + 1)] = d;
     rot_left(Dn, 4, p, p + 2, nd, cs, sn);
     rot_right(Dn, 4, p, 0, p, cs, sn);
@@ -650,7 +663,7 @@ int or_schedule(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w,
 /* ---------------------------------------------------------------------------
  * The reordering, Eq. (7).
  * ------------------------------------------------------------------------- */
-static void window_updates_naive(int64_t n, double* S, int64_t lds, double* Q, int64_t ldq,
+static void window_updates_naive(int64_t n, double* S, int64_t lds, double* Q, int64_t ldq, int64_t nq,
                                  int64_t j1, int64_t j2, const double* Z) {
   const int64_t k = j2 - j1;
   double* tmp = (double*)malloc(sizeof(double) * (size_t)k);
@@ -674,7 +687,7 @@ static void window_updates_naive(int64_t n, double* S, int64_t lds, double* Q, i
   }
   /* Q update (Q <- Q Q3): Q[:, j1:j2] <- Q[:, j1:j2] Z */
   if (Q) {
-    for (int64_t r = 0; r < n; ++r) {
+    for (int64_t r = 0; r < nq; ++r) {
       for (int64_t c = 0; c < k; ++c) {
         double acc = 0.0;
         for (int64_t l = 0; l < k; ++l) acc += IDX(Q, ldq, r, j1 + l) * Z[l + c * k];
@@ -689,11 +702,17 @@ static void window_updates_naive(int64_t n, double* S, int64_t lds, double* Q, i
 int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t ldq,
                int32_t* select, int64_t* m, int64_t w, int64_t max_windows,
                int64_t force_reject_at, int8_t* bmap_out, or_stats* st) {
+  return or_reorder_q(mode, n, S, lds, Q, ldq, n, select, m, w, max_windows, force_reject_at, bmap_out, st);
+}
+
+int or_reorder_q(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t ldq, int64_t nq,
+                 int32_t* select, int64_t* m, int64_t w, int64_t max_windows,
+                 int64_t force_reject_at, int8_t* bmap_out, or_stats* st) {
   if (mode != 0 && mode != 1) return -1;
   if (n < 0) return -2;
   if (n > 0 && S == NULL) return -3;
   if (lds < (n > 1 ? n : 1)) return -4;
-  if (Q && ldq < (n > 1 ? n : 1)) return -6;
+  if (Q && (nq < 0 || nq > n || ldq < (nq > 1 ? nq : 1))) return -6;
   if (n > 0 && select == NULL) return -7;
   if (m == NULL) return -8;
   if (w < 4) return -9;
@@ -726,7 +745,7 @@ int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t l
     if (mode == 0) {
       for (; done < k; ++done) {
         if (gswap + done == force_reject_at ||
-            or_swap(n, S, lds, tj[done], t1[done], t2[done], Q, ldq, Q ? n : 0)) {
+            or_swap(n, S, lds, tj[done], t1[done], t2[done], Q, ldq, Q ? nq : 0)) {
           rc = 1; break;
         }
         st->swaps_by_type[(t1[done] - 1) * 2 + (t2[done] - 1)]++;
@@ -746,11 +765,11 @@ int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t l
       }
       for (int64_t c = 0; c < kw; ++c)
         for (int64_t r = 0; r < kw; ++r) IDX(S, lds, j1 + r, j1 + c) = D[r + c * kw];
-      window_updates_naive(n, S, lds, Q, ldq, j1, j2, Z);
+      window_updates_naive(n, S, lds, Q, ldq, nq, j1, j2, Z);
     }
     st->swaps += done;
     st->windows++;
-    st->eq_flops += 2.0 * kw * kw * ((double)(n - j2) + (double)j1 + (Q ? (double)n : 0.0));
+    st->eq_flops += 2.0 * kw * kw * ((double)(n - j2) + (double)j1 + (Q ? (double)nq : 0.0));
     if (rc) {
       st->rejected_window = st->windows - 1;
       st->rejected_swap = gswap + done;
@@ -791,15 +810,20 @@ int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t l
  *   G2  other cases: the generalized Sylvester equation
  *         S11 R - L S22 = S12,  T11 R - L T22 = T12   (scale 1)
  *       by Gaussian elimination with complete pivoting on its Kronecker
- *       form (order 2 n1 n2); orthogonal bases of span[-R; I] (right) and
- *       span[-L; I] (left) by Householder QR.  G2b: if that pair fails the
- *       weak test (G3), T's block is re-triangularised (as xTGEX2 does) from
- *       the left or from the right, whichever leaves the smaller S block
- *       below the new leading block, and the test is applied to that.
- *   G3  weak stability test: the n1 x n2 block below the new leading block
- *       of each of S and T is at most max(20 eps max|block|, smlnum) of
- *       that matrix, else the swap is rejected (nothing is changed); passed
- *       blocks are set to exact zeros.
+ *       form (order 2 n1 n2); orthogonal bases V0 of span[-R; I] (right) and
+ *       U0 of span[-L; I] (left) by Householder QR.  Then, as xTGEX2 does on
+ *       every swap, T's block is re-triangularised both ways -- from the left
+ *       (U from a QR of the first n2 columns of T V0, V = V0) and from the
+ *       right (V completing the row space of the last n1 rows of U0^T T,
+ *       U = U0) -- so that T's block below the new leading block is zero to
+ *       working accuracy, and the variant whose S block there is smaller
+ *       (Frobenius norm; ties to the left variant) is kept.
+ *   G3  weak stability test: 1x1|1x1: |s21| and |t21| after the swap at most
+ *       max(20 eps ||block||_F, smlnum) of their matrix's block; other cases:
+ *       the kept variant's n1 x n2 S block below the new leading block at
+ *       most max(20 eps ||S block||_F, smlnum) (xTGEX2's test; T's is zero by
+ *       construction).  Otherwise the swap is rejected (nothing is changed);
+ *       passed blocks are set to exact zeros.
  *   G4  standard form: every 2x2 diagonal block of T is diagonal with
  *       t11 >= t22 > 0 (a 2x2 SVD applied to both matrices); the paired
  *       2x2 block of S is left general; a moved 1x1 block has t >= 0.  A moved 2x2 block whose pencil has
@@ -808,6 +832,12 @@ int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t l
  *       (Z-side) of each swap; a window accumulates UL and VR from I.
  *   G6  updates of a window [j1, j2): (S, T)[j1:j2, j2:n] <- UL^T (.),
  *       (S, T)[0:j1, j1:j2] <- (.) VR, Q[:, j1:j2] <- Q UL, Z[:, j1:j2] <- Z VR.
+ *   G7  basis signs: the swap's factors are fixed only up to a simultaneous
+ *       sign flip of a column of U and the same column of V (G1-G4 leave it
+ *       free; which variant G2 keeps can flip it).  Convention: the entry of
+ *       largest magnitude of every column of V (the first such entry) is
+ *       positive; U's column follows.  This makes the result a function of
+ *       the data rather than of rounding-level choices.
  * ========================================================================= */
 
 /* m x m matrices (m <= 4) column-major with ld 4 */
@@ -1012,9 +1042,13 @@ static int std_t22(const double* Tb, double* P, double* W) {
   return 0;
 }
 
+static int g_gswap_variant = 0;   /* diagnostics: 0 G1, 1 left variant kept, 2 right, -1 rejected */
+int or_gswap_last_variant(void) { return g_gswap_variant; }
+
 int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t j, int n1, int n2,
              double* Ql, int64_t ldq, int64_t nq, double* Zr, int64_t ldz, int64_t nz) {
   const int m = n1 + n2;
+  g_gswap_variant = 0;
   double A[16], B[16];
   memset(A, 0, sizeof(A));
   memset(B, 0, sizeof(B));
@@ -1050,7 +1084,7 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
     else or_lartg(bx0, bx1, &c2, &s2, &r2);
     U[0] = c2; U[1] = s2; U[4] = -s2; U[5] = c2;
   } else {
-    /* G2 */
+    /* G2: Sylvester bases, then both re-triangularisations of T's block (xTGEX2) */
     double A11[4] = {0}, A22[4] = {0}, A12[4] = {0}, B11[4] = {0}, B22[4] = {0}, B12[4] = {0};
     double R[4] = {0}, L[4] = {0};
     for (int c = 0; c < n1; ++c)
@@ -1063,7 +1097,7 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
     for (int c = 0; c < n2; ++c)
       for (int r = 0; r < n1; ++r) { A12[r + 2 * c] = A[r + 4 * (n1 + c)]; B12[r + 2 * c] = B[r + 4 * (n1 + c)]; }
     or_gsylv(n1, n2, A11, A22, A12, B11, B22, B12, R, L);
-    double Mr[16], Ml[16];
+    double Mr[16], Ml[16], U0[16], V0[16];
     memset(Mr, 0, sizeof(Mr));
     memset(Ml, 0, sizeof(Ml));
     for (int c = 0; c < n2; ++c) {
@@ -1071,58 +1105,44 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
       Mr[(n1 + c) + 4 * c] = 1.0;
       Ml[(n1 + c) + 4 * c] = 1.0;
     }
-    sm_qr_basis(Mr, m, n2, V);
-    sm_qr_basis(Ml, m, n2, U);
+    sm_qr_basis(Mr, m, n2, V0);
+    sm_qr_basis(Ml, m, n2, U0);
+    /* from the left: Uq from a QR of the first n2 columns of T V0 */
+    double I4[16], TV[16], UT[16], Uq[16], H[16], Vr[16], Mq[16], Mrr[16];
+    sm_eye(I4, m);
+    sm_congruence(I4, B, V0, TV, m);
+    memset(Mq, 0, sizeof(Mq));
+    for (int c = 0; c < n2; ++c)
+      for (int r = 0; r < m; ++r) Mq[r + 4 * c] = TV[r + 4 * c];
+    sm_qr_basis(Mq, m, n2, Uq);
+    /* from the right: Vr = [complement of the row space of rows n2.. of U0^T T, that row space] */
+    sm_congruence(U0, B, I4, UT, m);
+    memset(Mrr, 0, sizeof(Mrr));
+    for (int c = 0; c < n1; ++c)
+      for (int r = 0; r < m; ++r) Mrr[r + 4 * c] = UT[(n2 + c) + 4 * r];
+    sm_qr_basis(Mrr, m, n1, H);
+    memset(Vr, 0, sizeof(Vr));
+    for (int c = 0; c < n2; ++c)
+      for (int r = 0; r < m; ++r) Vr[r + 4 * c] = H[r + 4 * (n1 + c)];
+    for (int c = 0; c < n1; ++c)
+      for (int r = 0; r < m; ++r) Vr[r + 4 * (n2 + c)] = H[r + 4 * c];
+    double Aq[16], Ar[16];
+    sm_congruence(Uq, A, V0, Aq, m);
+    sm_congruence(U0, A, Vr, Ar, m);
+    const double rq = lowblock_fro(Aq, n1, n2), rr = lowblock_fro(Ar, n1, n2);
+    if (rq <= rr) { memcpy(U, Uq, sizeof(Uq)); memcpy(V, V0, sizeof(V0)); }
+    else { memcpy(U, U0, sizeof(U0)); memcpy(V, Vr, sizeof(Vr)); }
+    g_gswap_variant = rq <= rr ? 1 : 2;
   }
-  /* trial */
   double An[16], Bn[16];
   sm_congruence(U, A, V, An, m);
   sm_congruence(U, B, V, Bn, m);
-  if (!(n1 == 1 && n2 == 1) && !(lowblock_fro(An, n1, n2) <= threshA && lowblock_fro(Bn, n1, n2) <= threshB)) {
-      /* G2b (xTGEX2): make T's block below the new leading block zero to working accuracy,
-       * either from the left (U from a QR of the first n2 columns of T V) or from the right (V
-       * completing the row space of the last n1 rows of U^T T); keep the variant whose S block
-       * below the new leading block is smaller (Frobenius norm). */
-      double Uq[16], Vr[16], TV[16], UT[16], Mq[16], Mrr[16], H[16], I4[16];
-      sm_eye(I4, m);
-      sm_congruence(I4, B, V, TV, m);                 /* T V */
-      sm_congruence(U, B, I4, UT, m);                 /* U^T T */
-      memset(Mq, 0, sizeof(Mq));
-      memset(Mrr, 0, sizeof(Mrr));
-      for (int c = 0; c < n2; ++c)
-        for (int r = 0; r < m; ++r) Mq[r + 4 * c] = TV[r + 4 * c];
-      for (int c = 0; c < n1; ++c)
-        for (int r = 0; r < m; ++r) Mrr[r + 4 * c] = UT[(n2 + c) + 4 * r];
-      sm_qr_basis(Mq, m, n2, Uq);
-      sm_qr_basis(Mrr, m, n1, H);
-      /* V_r: the complement of the row space first, then the row space */
-      memset(Vr, 0, sizeof(Vr));
-      for (int c = 0; c < n2; ++c)
-        for (int r = 0; r < m; ++r) Vr[r + 4 * c] = H[r + 4 * (n1 + c)];
-      for (int c = 0; c < n1; ++c)
-        for (int r = 0; r < m; ++r) Vr[r + 4 * (n2 + c)] = H[r + 4 * c];
-      double Aq[16], Ar[16];
-      sm_congruence(Uq, A, V, Aq, m);
-      sm_congruence(U, A, Vr, Ar, m);
-      double rq = 0.0, rr = 0.0;
-      for (int c = 0; c < n2; ++c)
-        for (int r = n2; r < m; ++r) { rq += Aq[r + 4 * c] * Aq[r + 4 * c]; rr += Ar[r + 4 * c] * Ar[r + 4 * c]; }
-      if (rq <= rr) memcpy(U, Uq, sizeof(Uq));
-      else memcpy(V, Vr, sizeof(Vr));
-
-    sm_congruence(U, A, V, An, m);
-    sm_congruence(U, B, V, Bn, m);
+  /* G3 */
+  const double resA = lowblock_fro(An, n1, n2), resB = lowblock_fro(Bn, n1, n2);
+  if (n1 == 1 && n2 == 1 ? !(resA <= threshA && resB <= threshB) : !(resA <= threshA)) {
+    g_gswap_variant = -1;
+    return 1;
   }
-  /* G3: Frobenius norm of the block below the new leading n2 x n2 block */
-  double resA = 0.0, resB = 0.0;
-  for (int c = 0; c < n2; ++c)
-    for (int r = n2; r < m; ++r) {
-      resA += An[r + 4 * c] * An[r + 4 * c];
-      resB += Bn[r + 4 * c] * Bn[r + 4 * c];
-    }
-  resA = sqrt(resA);
-  resB = sqrt(resB);
-  if (!(resA <= threshA && resB <= threshB)) return 1;
   for (int c = 0; c < n2; ++c)
     for (int r = n2; r < m; ++r) { An[r + 4 * c] = 0.0; Bn[r + 4 * c] = 0.0; }
   /* G4: standard form of each new 2x2 block */
@@ -1133,7 +1153,7 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
     const int p = pos[q];
     double Tb[4] = {Bn[p + 4 * p], Bn[(p + 1) + 4 * p], Bn[p + 4 * (p + 1)], Bn[(p + 1) + 4 * (p + 1)]};
     double P2[4], W2[4];
-    if (std_t22(Tb, P2, W2)) return 1;
+    if (std_t22(Tb, P2, W2)) { g_gswap_variant = -1; return 1; }
     double Pm[16], Wm[16];
     sm_eye(Pm, m);
     sm_eye(Wm, m);
@@ -1153,7 +1173,7 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
     const double e11 = An[p + 4 * p] / t11, e12 = An[p + 4 * (p + 1)] / t11;
     const double e21 = An[(p + 1) + 4 * p] / t22, e22 = An[(p + 1) + 4 * (p + 1)] / t22;
     const double h = 0.5 * (e11 - e22);
-    if (!(h * h + e12 * e21 < 0.0)) return 1;
+    if (!(h * h + e12 * e21 < 0.0)) { g_gswap_variant = -1; return 1; }
   }
   /* G4: a new 1x1 block has t >= 0 (negate its row of the pencil and its column of U) */
   int one[2], no = 0;
@@ -1166,6 +1186,22 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
       for (int r = 0; r < m; ++r) U[r + 4 * p] = -U[r + 4 * p];
     }
   }
+  /* G7: the largest-magnitude entry of every column of V is positive (U's column follows;
+   * the block entries change as D An D, D Bn D with D = diag(+-1)) */
+  double d[4] = {1.0, 1.0, 1.0, 1.0};
+  for (int c = 0; c < m; ++c) {
+    int im = 0;
+    for (int r = 1; r < m; ++r)
+      if (fabs(V[r + 4 * c]) > fabs(V[im + 4 * c])) im = r;
+    if (V[im + 4 * c] < 0.0) d[c] = -1.0;
+  }
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < m; ++r) {
+      U[r + 4 * c] *= d[c];
+      V[r + 4 * c] *= d[c];
+      An[r + 4 * c] *= d[r] * d[c];
+      Bn[r + 4 * c] *= d[r] * d[c];
+    }
   /* commit */
   apply_left_small(S, lds, j, m, j + m, nt, U);
   apply_left_small(T, ldt, j, m, j + m, nt, U);
@@ -1315,4 +1351,245 @@ int or_greorder(int mode, int64_t n, double* S, int64_t lds, double* T, int64_t 
   free(bmap); free(selrow);
   sched_free(&sc);
   return rc;
+}
+
+/* ===========================================================================
+ * Eigenvectors.  PAPER.md Eq. (5): vectors y_i with
+ * (S - lambda_i I) y_i = 0 for the quasi-triangular S, and Eq. (6):
+ * the back-transform x_i = Q y_i; "the computations must be protected against
+ * floating-point overflow".  Readings E1-E6:
+ *   E1  columns: one per selected 1x1 block (real lambda = s_kk), two per
+ *       selected 2x2 block [a b; c a] (bc < 0, lambda = a + i w, w =
+ *       sqrt|b| sqrt|c|): the real and imaginary parts of the eigenvector of
+ *       lambda, in the order of the blocks.
+ *   E2  the eigenvector's own block (LAPACK xTREVC): real y_k = 1; complex
+ *       (y_k, y_k+1) = (1, i w / b) if |b| >= |c|, else (-w / c, i).
+ *       Entries below the block are 0.
+ *   E3  rows above the block, bottom to top over S's block structure: a 1x1
+ *       row i solves (s_ii - lambda) y_i = r_i, a 2x2 block the 2x2 (real or
+ *       complex) system (S_blk - lambda I) y_blk = r_blk by Gaussian
+ *       elimination with complete pivoting; a pivot below smin = max(eps
+ *       (|Re lambda| + |Im lambda|), DBL_MIN / eps) is replaced by smin
+ *       (xLALN2's perturbation); then r_l -= S[l, blk] y_blk for the rows l
+ *       above.  Complex arithmetic on (re, im) pairs.
+ *   E4  overflow protection (SPEC eigvec: Omega = 2^500, power-of-two
+ *       scalings): the column (pair) carries a scale 2^-e; before a division
+ *       whose result would exceed Omega, and before an update whose result
+ *       could exceed Omega (max_l |r_l| + max_l |S[l, blk]| |y_blk| > Omega),
+ *       the whole column is multiplied by the smallest power of two 2^-s that
+ *       makes it safe; every stored value stays <= Omega.
+ *   E5  normalisation (xTREVC): the column (pair) is divided by
+ *       max_i (|re_i| + |im_i|) (multiplied by its reciprocal).
+ *   E6  back-transform: X = Q Y (naive triple loop) before the normalisation.
+ * ========================================================================= */
+#define OR_OMEGA 3.273390607896142e+150   /* 2^500 */
+
+/* smallest s >= 0 with v * 2^-s <= lim (v, lim > 0) */
+static int pow2_steps(double v, double lim) {
+  int s = 0;
+  while (v > lim) { v *= 0.5; ++s; }
+  return s;
+}
+
+/* complex helpers on (re, im) pairs */
+static double cabs1(double re, double im) { return fabs(re) + fabs(im); }
+static void cdiv(double ar, double ai, double br, double bi, double* cr, double* ci) {
+  /* (ar + i ai) / (br + i bi), Smith's algorithm */
+  if (fabs(br) >= fabs(bi)) {
+    const double r = bi / br, d = br + bi * r;
+    *cr = (ar + ai * r) / d;
+    *ci = (ai - ar * r) / d;
+  } else {
+    const double r = br / bi, d = bi + br * r;
+    *cr = (ar * r + ai) / d;
+    *ci = (ai * r - ar) / d;
+  }
+}
+
+/* Solve the nb x nb (nb = 1, 2) complex system (B - (wr + i wi) I) y = r, B real (ld 2),
+ * by Gaussian elimination with complete pivoting; pivots below smin are replaced by smin.
+ * Returns the largest |y| (cabs1). */
+static double small_csolve(int nb, const double* B, double wr, double wi, double smin, const double* rr,
+                           const double* ri, double* yr, double* yi) {
+  if (nb == 1) {
+    double dr = B[0] - wr, di = -wi;
+    if (cabs1(dr, di) < smin) { dr = smin; di = 0.0; }
+    cdiv(rr[0], ri[0], dr, di, &yr[0], &yi[0]);
+    return cabs1(yr[0], yi[0]);
+  }
+  /* M = B - lambda I (2x2 complex), complete pivoting */
+  double mr[2][2] = {{B[0] - wr, B[2]}, {B[1], B[3] - wr}};
+  double mi[2][2] = {{-wi, 0.0}, {0.0, -wi}};
+  double br[2] = {rr[0], rr[1]}, bi[2] = {ri[0], ri[1]};
+  int pr = 0, pc = 0;
+  double best = -1.0;
+  for (int c = 0; c < 2; ++c)
+    for (int r = 0; r < 2; ++r)
+      if (cabs1(mr[r][c], mi[r][c]) > best) { best = cabs1(mr[r][c], mi[r][c]); pr = r; pc = c; }
+  if (pr == 1) {
+    for (int c = 0; c < 2; ++c) {
+      double t = mr[0][c]; mr[0][c] = mr[1][c]; mr[1][c] = t;
+      t = mi[0][c]; mi[0][c] = mi[1][c]; mi[1][c] = t;
+    }
+    double t = br[0]; br[0] = br[1]; br[1] = t;
+    t = bi[0]; bi[0] = bi[1]; bi[1] = t;
+  }
+  if (pc == 1) {
+    for (int r = 0; r < 2; ++r) {
+      double t = mr[r][0]; mr[r][0] = mr[r][1]; mr[r][1] = t;
+      t = mi[r][0]; mi[r][0] = mi[r][1]; mi[r][1] = t;
+    }
+  }
+  if (cabs1(mr[0][0], mi[0][0]) < smin) { mr[0][0] = smin; mi[0][0] = 0.0; }
+  double lr, li;                                   /* l = m10 / m00 */
+  cdiv(mr[1][0], mi[1][0], mr[0][0], mi[0][0], &lr, &li);
+  double ur = mr[1][1] - (lr * mr[0][1] - li * mi[0][1]);
+  double ui = mi[1][1] - (lr * mi[0][1] + li * mr[0][1]);
+  const double b1r = br[1] - (lr * br[0] - li * bi[0]);
+  const double b1i = bi[1] - (lr * bi[0] + li * br[0]);
+  if (cabs1(ur, ui) < smin) { ur = smin; ui = 0.0; }
+  double x1r, x1i, x0r, x0i;
+  cdiv(b1r, b1i, ur, ui, &x1r, &x1i);
+  const double tr = br[0] - (mr[0][1] * x1r - mi[0][1] * x1i);
+  const double ti = bi[0] - (mr[0][1] * x1i + mi[0][1] * x1r);
+  cdiv(tr, ti, mr[0][0], mi[0][0], &x0r, &x0i);
+  if (pc == 1) { yr[0] = x1r; yi[0] = x1i; yr[1] = x0r; yi[1] = x0i; }
+  else { yr[0] = x0r; yi[0] = x0i; yr[1] = x1r; yi[1] = x1i; }
+  return dmax(cabs1(yr[0], yi[0]), cabs1(yr[1], yi[1]));
+}
+
+int or_eig_count(int64_t n, const double* S, int64_t lds, const int32_t* select, int64_t* ncols) {
+  if (n < 0) return -1;
+  if (n > 0 && (S == NULL || select == NULL)) return -2;
+  int8_t* bmap = (int8_t*)malloc((size_t)(n > 0 ? n : 1));
+  if (n > 0 && or_scan(n, S, lds, bmap)) { free(bmap); return -2; }
+  int64_t c = 0;
+  for (int64_t i = 0; i < n;) {
+    const int bs = bmap[i] == 1 ? 2 : 1;
+    if (select[i] || (bs == 2 && select[i + 1])) c += bs;
+    i += bs;
+  }
+  free(bmap);
+  *ncols = c;
+  return 0;
+}
+
+int or_eigvec(int64_t n, const double* S, int64_t lds, const double* Q, int64_t ldq, const int32_t* select,
+              double* X, int64_t ldx, int32_t* scale_exp) {
+  if (n < 0) return -1;
+  if (n == 0) return 0;
+  if (S == NULL || lds < n) return -2;
+  if (Q != NULL && ldq < n) return -4;
+  if (select == NULL) return -6;
+  if (X == NULL || ldx < n) return -7;
+  int8_t* bmap = (int8_t*)malloc((size_t)n);
+  if (or_scan(n, S, lds, bmap)) { free(bmap); return -2; }
+  const double eps = DBL_EPSILON, smlnum = DBL_MIN / DBL_EPSILON;
+  double* yr = (double*)malloc(sizeof(double) * (size_t)n);
+  double* yi = (double*)malloc(sizeof(double) * (size_t)n);
+  int64_t col = 0;
+  for (int64_t k = 0; k < n;) {
+    const int bs = bmap[k] == 1 ? 2 : 1;
+    if (!(select[k] || (bs == 2 && select[k + 1]))) { k += bs; continue; }
+    /* E1/E2: lambda and the block's own entries */
+    double wr, wi = 0.0;
+    for (int64_t i = 0; i < n; ++i) { yr[i] = 0.0; yi[i] = 0.0; }
+    if (bs == 1) {
+      wr = IDX(S, lds, k, k);
+      yr[k] = 1.0;
+    } else {
+      const double b = IDX(S, lds, k, k + 1), c = IDX(S, lds, k + 1, k);
+      wr = IDX(S, lds, k, k);
+      wi = sqrt(fabs(b)) * sqrt(fabs(c));
+      if (fabs(b) >= fabs(c)) { yr[k] = 1.0; yi[k + 1] = wi / b; }
+      else { yr[k] = -wi / c; yi[k + 1] = 1.0; }
+    }
+    const double smin = dmax(eps * (fabs(wr) + fabs(wi)), smlnum);
+    int e = 0;                                     /* the column holds (true vector) * 2^-e */
+    /* right-hand side of the rows above: r_l = -S[l, k:k+bs] y_blk */
+    for (int64_t l = 0; l < k; ++l)
+      for (int q = 0; q < bs; ++q) {
+        yr[l] -= IDX(S, lds, l, k + q) * yr[k + q];
+        yi[l] -= IDX(S, lds, l, k + q) * yi[k + q];
+      }
+    /* E3/E4: blocks above, bottom to top */
+    int64_t i = k;
+    while (i > 0) {
+      const int nb = (i >= 2 && bmap[i - 1] == 2) ? 2 : 1;
+      i -= nb;
+      double B[4] = {IDX(S, lds, i, i), 0.0, 0.0, 0.0};
+      if (nb == 2) {
+        B[1] = IDX(S, lds, i + 1, i); B[2] = IDX(S, lds, i, i + 1); B[3] = IDX(S, lds, i + 1, i + 1);
+      }
+      double rr[2] = {yr[i], nb == 2 ? yr[i + 1] : 0.0}, ri[2] = {yi[i], nb == 2 ? yi[i + 1] : 0.0};
+      double sr[2], si[2];
+      double ymax = small_csolve(nb, B, wr, wi, smin, rr, ri, sr, si);
+      if (!(ymax <= OR_OMEGA)) {
+        /* scale the column so that the solve stays below Omega (the right-hand side is
+         * scaled and the small system solved again: exact powers of two) */
+        double rmax = dmax(cabs1(rr[0], ri[0]), nb == 2 ? cabs1(rr[1], ri[1]) : 0.0);
+        int s = 1;
+        if (ymax == ymax && ymax < 1e308) s = pow2_steps(ymax, OR_OMEGA);
+        else s = pow2_steps(rmax, OR_OMEGA * smin) + 1;
+        for (;;) {
+          const double f = ldexp(1.0, -s);
+          double r2r[2] = {rr[0] * f, rr[1] * f}, r2i[2] = {ri[0] * f, ri[1] * f};
+          ymax = small_csolve(nb, B, wr, wi, smin, r2r, r2i, sr, si);
+          if (ymax <= OR_OMEGA) break;
+          ++s;
+        }
+        const double f = ldexp(1.0, -s);
+        for (int64_t l = 0; l < n; ++l) { yr[l] *= f; yi[l] *= f; }
+        e += s;
+      }
+      for (int q = 0; q < nb; ++q) { yr[i + q] = sr[q]; yi[i + q] = si[q]; }
+      if (i == 0) break;
+      /* update of the rows above: protect against overflow of r_l - S[l, blk] y_blk */
+      double rmax = 0.0, cmax = 0.0;
+      for (int64_t l = 0; l < i; ++l) {
+        rmax = dmax(rmax, cabs1(yr[l], yi[l]));
+        for (int q = 0; q < nb; ++q) cmax = dmax(cmax, fabs(IDX(S, lds, l, i + q)));
+      }
+      const double grow = rmax + (double)nb * cmax * ymax;
+      if (grow > OR_OMEGA) {
+        const int s = pow2_steps(grow, OR_OMEGA);
+        const double f = ldexp(1.0, -s);
+        for (int64_t l = 0; l < n; ++l) { yr[l] *= f; yi[l] *= f; }
+        e += s;
+      }
+      for (int64_t l = 0; l < i; ++l)
+        for (int q = 0; q < nb; ++q) {
+          yr[l] -= IDX(S, lds, l, i + q) * yr[i + q];
+          yi[l] -= IDX(S, lds, l, i + q) * yi[i + q];
+        }
+    }
+    /* E6: back-transform (rows of Y below k + bs are zero) */
+    double* xr = &IDX(X, ldx, 0, col);
+    double* xi = bs == 2 ? &IDX(X, ldx, 0, col + 1) : NULL;
+    if (Q) {
+      for (int64_t r = 0; r < n; ++r) {
+        double ar = 0.0, ai = 0.0;
+        for (int64_t l = 0; l < k + bs; ++l) {
+          ar += IDX(Q, ldq, r, l) * yr[l];
+          ai += IDX(Q, ldq, r, l) * yi[l];
+        }
+        xr[r] = ar;
+        if (xi) xi[r] = ai;
+      }
+    } else {
+      for (int64_t r = 0; r < n; ++r) { xr[r] = yr[r]; if (xi) xi[r] = yi[r]; }
+    }
+    /* E5: normalisation */
+    double emax = 0.0;
+    for (int64_t r = 0; r < n; ++r) emax = dmax(emax, fabs(xr[r]) + (xi ? fabs(xi[r]) : 0.0));
+    if (emax > 0.0) {
+      const double rem = 1.0 / emax;
+      for (int64_t r = 0; r < n; ++r) { xr[r] *= rem; if (xi) xi[r] *= rem; }
+    }
+    if (scale_exp) { scale_exp[col] = e; if (bs == 2) scale_exp[col + 1] = e; }
+    col += bs;
+    k += bs;
+  }
+  free(yr); free(yi); free(bmap);
+  return 0;
 }

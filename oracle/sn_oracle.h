@@ -64,6 +64,11 @@ int or_sylv(int n1, int n2, const double* T11, const double* T22, const double* 
 int or_swap(int64_t nt, double* T, int64_t ldt, int64_t j, int n1, int n2,
             double* Qm, int64_t ldq, int64_t nq);
 
+/* Diagnostics of the last or_swap call (not thread-safe): 0 accepted, 1 rejected by the
+ * weak stability test (c4 #5), 2 rejected because a moved 2x2 block would split into two
+ * real eigenvalues (reading R6). */
+int or_swap_last_reject(void);
+
 /* ---- structure and selection (row a1 of SURVEY §8a) ---- */
 
 /* Block map: bmap[i] = 0 (1x1 block), 1 (first row of a 2x2), 2 (second row).
@@ -115,6 +120,13 @@ int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t l
                int32_t* select, int64_t* m, int64_t w, int64_t max_windows,
                int64_t force_reject_at, int8_t* bmap_out, or_stats* st);
 
+/* The same with Q of nq <= n rows (ld >= nq): rows of Q are updated independently
+ * (Q <- Q Q3 row by row), so a row sample of Q gives exactly those rows of the full
+ * result -- prefix parity at sizes where a full copy of Q does not fit. */
+int or_reorder_q(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t ldq, int64_t nq,
+                 int32_t* select, int64_t* m, int64_t w, int64_t max_windows,
+                 int64_t force_reject_at, int8_t* bmap_out, or_stats* st);
+
 /* ---- generalized reordering (Eq. (7) right form; Table 1
  * P:216).  Readings G1-G6 in sn_oracle.c and DESIGN.md §3. ----
  *
@@ -134,6 +146,10 @@ int or_gsylv(int n1, int n2, const double* A11, const double* A22, const double*
 int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t j, int n1, int n2,
              double* Ql, int64_t ldq, int64_t nq, double* Zr, int64_t ldz, int64_t nz);
 
+/* Diagnostics of the last or_gswap call (not thread-safe): 0 a 1x1|1x1 swap (G1), 1 the
+ * left re-triangularisation kept (G2), 2 the right one kept, -1 rejected (G3/G4). */
+int or_gswap_last_variant(void);
+
 /* Generalized reordering (S, T) = Q3 (Ŝ, T̂) Z3^T, Q <- Q Q3, Z <- Z Z3 (Q, Z may be
  * NULL), with the schedule of or_reorder (it depends only on the block map of S and
  * the selection).  mode 0 = swaps applied to the full matrices, 1 = per window
@@ -143,6 +159,22 @@ int or_greorder(int mode, int64_t n, double* S, int64_t lds, double* T, int64_t 
                 double* Q, int64_t ldq, double* Z, int64_t ldz, int32_t* select, int64_t* m,
                 int64_t w, int64_t max_windows, int64_t force_reject_at, int8_t* bmap_out,
                 or_stats* st);
+
+/* ---- eigenvectors (Eq. (5)-(6); overflow protection P:104-105).
+ * Readings E1-E6 in sn_oracle.c and DESIGN.md §3.2.
+ *
+ * Number of columns for a selection: one per selected 1x1 block, two per selected 2x2
+ * block (a 2x2 block is selected if either of its rows is).  Returns 0 or -2 (S not
+ * quasi-triangular). */
+int or_eig_count(int64_t n, const double* S, int64_t lds, const int32_t* select, int64_t* ncols);
+
+/* Right eigenvectors of the selected blocks of S (standardised quasi-triangular), columns
+ * in block order (2x2: real part, imaginary part), back-transformed X = Q Y if Q != NULL,
+ * each column (pair) normalised so that max_i(|re_i| + |im_i|) = 1.  X: n x ncols, ld ldx.
+ * scale_exp (may be NULL): per column the e of the power-of-two scaling 2^-e the overflow
+ * protection applied (E4).  Returns 0 or -i for argument i. */
+int or_eigvec(int64_t n, const double* S, int64_t lds, const double* Q, int64_t ldq, const int32_t* select,
+              double* X, int64_t ldx, int32_t* scale_exp);
 
 #ifdef __cplusplus
 }

@@ -48,7 +48,7 @@ struct DevBuf {
 };
 
 struct Workspace {
-  DevBuf wins, pool, prefix, status, kwork, ctl, Z, zr, sub, bad;
+  DevBuf wins, pool, prefix, status, kwork, ctl, recs, Z, zr, sub, bad;
   DevBuf hS, hQ;                   // device staging of host-buffer calls (kept between calls)
   std::vector<cudaEvent_t> prof;   // event pool for opts.profile
   cudaStream_t sB = nullptr, sC = nullptr, sU = nullptr;   // sU: host->device upload of Q
@@ -87,6 +87,18 @@ int ensure_runtime(Workspace& ws) {
   int dev = 0;
   CK(cudaGetDevice(&dev));
   if (ws.device != dev) {
+    if (ws.device >= 0) {
+      // the buffers, streams and events belong to the previous device: release them there
+      cudaSetDevice(ws.device);
+      for (DevBuf* b : {&ws.wins, &ws.pool, &ws.prefix, &ws.status, &ws.kwork, &ws.ctl, &ws.recs, &ws.Z, &ws.zr,
+                        &ws.sub, &ws.bad, &ws.hS, &ws.hQ}) {
+        if (b->p) cudaFree(b->p);
+        b->p = nullptr;
+        b->cap = 0;
+      }
+      for (auto e : ws.prof) cudaEventDestroy(e);
+      ws.prof.clear();
+    }
     if (ws.sB) {
       cudaStreamDestroy(ws.sB);
       cudaStreamDestroy(ws.sC);
@@ -103,6 +115,7 @@ int ensure_runtime(Workspace& ws) {
       cudaEventDestroy(ws.ev0); cudaEventDestroy(ws.ev1);
       cudaEventDestroy(ws.evJoin); cudaEventDestroy(ws.evJoinC);
     }
+    if (ws.device >= 0) CK(cudaSetDevice(dev));
     // Priorities: the critical path (window kernel -> critical strips -> next window kernel)
     // runs on the highest-priority stream so that its CTAs are dispatched ahead of the queued
     // update strips of the other streams (lowest priority).
@@ -173,12 +186,14 @@ int structure_from_sub(int64_t n, const uint8_t* sub, const int32_t* select, int
   return 0;
 }
 
-void final_blocks(const Plan& P, const std::vector<int64_t>& sorted, const Control& ctl, const int32_t* status,
-                  int64_t n, const int8_t* bmap, const int8_t* selrow, std::vector<uint8_t>& fsz,
-                  std::vector<uint8_t>& fsel, int64_t* executed_out, int64_t* swaps_out, int64_t sbt[4]) {
+void final_blocks(const Plan& P, const std::vector<int64_t>& sorted, bool aborted, const int32_t* status,
+                  const WinRec* recs, int64_t n, const int8_t* bmap, const int8_t* selrow, std::vector<uint8_t>& fsz,
+                  std::vector<uint8_t>& fsel, int64_t* executed_out, int64_t* swaps_out, int64_t sbt[4],
+                  int64_t* rej_sorted) {
   const int64_t nw = (int64_t)P.wins.size();
   int64_t executed = nw, swaps = 0;
-  if (!ctl.abort) {
+  if (rej_sorted) *rej_sorted = -1;
+  if (!aborted) {
     fsz = P.final_sz; fsel = P.final_sel;
     for (const auto& w : P.wins) {
       swaps += w.nswap;
@@ -194,19 +209,22 @@ void final_blocks(const Plan& P, const std::vector<int64_t>& sorted, const Contr
     std::vector<int64_t> pos_of(nw);
     for (int64_t i = 0; i < nw; ++i) pos_of[sorted[i]] = i;
     executed = 0;
-    for (int64_t t = 0; t < nw; ++t) {
+    for (int64_t t = 0; t < nw; ++t) {   // schedule order: windows of one level are disjoint
       const WindowPlan& w = P.wins[t];
-      const int32_t stt = status[pos_of[t]];
+      const int64_t si = pos_of[t];
+      const int32_t stt = status[si];
       if (stt == kWinDone) {
         partition(fsz, fsel, w.top, w.nblk, P.pool.data() + w.pool, P.pool.data() + w.pool + w.nblk);
         swaps += w.nswap;
         for (int q = 0; q < 4; ++q) sbt[q] += w.swaps_by_type[q];
         ++executed;
       } else if (stt == kWinPartial) {
-        std::memcpy(fsz.data() + w.top, ctl.rej_sz, (size_t)w.nblk);
-        std::memcpy(fsel.data() + w.top, ctl.rej_sel, (size_t)w.nblk);
-        swaps += ctl.rej_swaps_done;
+        // this window's own record: several windows of the rejecting level may be partial
+        std::memcpy(fsz.data() + w.top, recs[si].sz, (size_t)w.nblk);
+        std::memcpy(fsel.data() + w.top, recs[si].sel, (size_t)w.nblk);
+        swaps += recs[si].done;
         ++executed;
+        if (rej_sorted && *rej_sorted < 0) *rej_sorted = si;   // first in schedule order
       }
     }
   }
@@ -254,6 +272,12 @@ int run(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64_t 
   CK(cudaEventRecord(ws.evIn, sUser));
   CK(cudaStreamWaitEvent(ws.sH, ws.evIn, 0));
   const int rc = run_on(o, n, S, ldS, Q, ldQ, select, m, bmap_out, st, ws.sH, q_ready, ho);
+  // join the library's other streams on every exit path (an error return may leave Q updates
+  // or remaining strips queued on them): the caller's stream then waits for all of it
+  cudaEventRecord(ws.evJoin, ws.sB);
+  cudaStreamWaitEvent(ws.sH, ws.evJoin, 0);
+  cudaEventRecord(ws.evJoinC, ws.sC);
+  cudaStreamWaitEvent(ws.sH, ws.evJoinC, 0);
   cudaEventRecord(ws.evOut, ws.sH);
   cudaStreamWaitEvent(sUser, ws.evOut, 0);
   return rc;
@@ -386,6 +410,7 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
   CK(ws.status.ensure(sizeof(int32_t) * nw));
   CK(ws.kwork.ensure(sizeof(int32_t) * nw));
   CK(ws.ctl.ensure(sizeof(Control)));
+  CK(ws.recs.ensure(sizeof(WinRec) * nw));
   CK(ws.Z.ensure(sizeof(double) * (size_t)kZslot * (size_t)(kZgen * maxper)));
   CK(ws.zr.ensure(sizeof(int16_t) * (size_t)kZrange * (size_t)(kZgen * maxper)));
   CK(cudaMemcpyAsync(ws.wins.p, wd.data(), sizeof(WinDev) * nw, cudaMemcpyHostToDevice, sA));
@@ -393,6 +418,7 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
   CK(cudaMemcpyAsync(ws.prefix.p, pref.data(), sizeof(int32_t) * pref.size(), cudaMemcpyHostToDevice, sA));
   CK(cudaMemsetAsync(ws.status.p, 0, sizeof(int32_t) * nw, sA));
   CK(cudaMemsetAsync(ws.ctl.p, 0, sizeof(Control), sA));
+  CK(cudaMemsetAsync(ws.recs.p, 0, sizeof(WinRec) * nw, sA));
 
   const int mt = o.window <= 64 ? 64 : (o.window <= 128 ? 128 : 256);
   WinDev* dw = (WinDev*)ws.wins.p;
@@ -442,6 +468,7 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
     wa.wins = dw + a; wa.nwin = (int32_t)cnt; wa.base = (int32_t)a;
     wa.pool = (const uint8_t*)ws.pool.p; wa.S = S; wa.ldS = ldS; wa.Z = dZ;
     wa.status = dstatus; wa.ctl = dctl; wa.zrange = (int16_t*)ws.zr.p; wa.kwork = (int32_t*)ws.kwork.p;
+    wa.recs = (WinRec*)ws.recs.p; wa.level = (int32_t)l;
     wa.tprof = dtp;
     wa.force_order = o.force_reject_window; wa.force_swap = (int32_t)o.force_reject_swap;
     int pe = prof_begin(0, sA);
@@ -545,15 +572,18 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
   // ---- outputs: final block list
   std::vector<uint8_t> fsz, fsel;
   std::vector<int32_t> status;
-  int64_t executed = nw, swaps = 0;
+  std::vector<WinRec> recs;
+  int64_t executed = nw, swaps = 0, rej = -1;
   double eqf = 0.0;
   int64_t sbt[4] = {0, 0, 0, 0};
   if (ctl.abort) {
     status.resize(nw);
+    recs.resize(nw);
     CK(cudaMemcpy(status.data(), dstatus, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(recs.data(), ws.recs.p, sizeof(WinRec) * nw, cudaMemcpyDeviceToHost));
   }
-  final_blocks(P, sorted, ctl, ctl.abort ? status.data() : nullptr, n, bmap.data(), selrow.data(), fsz, fsel,
-               &executed, &swaps, sbt);
+  final_blocks(P, sorted, ctl.abort != 0, ctl.abort ? status.data() : nullptr, recs.data(), n, bmap.data(),
+               selrow.data(), fsz, fsel, &executed, &swaps, sbt, &rej);
   double fk[5] = {0, 0, 0, 0, 0}, bk[5] = {0, 0, 0, 0, 0}, fx[5] = {0, 0, 0, 0, 0};
   std::vector<int32_t> kwork(nw, 0);
   CK(cudaMemcpy(kwork.data(), ws.kwork.p, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
@@ -585,11 +615,11 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
     st->inner_windows = P.ninner;
     st->rejected_window = -1;
     st->rejected_row = -1;
-    if (ctl.abort) {
-      st->rejected_window = P.wins[sorted[ctl.rej_window]].order;
-      st->rejected_row = ctl.rej_row;
-      st->rejected_n1 = ctl.rej_n1;
-      st->rejected_n2 = ctl.rej_n2;
+    if (ctl.abort && rej >= 0) {
+      st->rejected_window = P.wins[sorted[rej]].order;
+      st->rejected_row = recs[rej].row;
+      st->rejected_n1 = recs[rej].n1;
+      st->rejected_n2 = recs[rej].n2;
     }
     st->eq_flops = eqf;
     st->ms_schedule = t_plan - t_start;
@@ -643,7 +673,7 @@ const char* sn_version(void) { return "sn_b200 0.1 (sm_100a)"; }
 void sn_release_workspace(void) {
   std::lock_guard<std::mutex> lock(sn::g_mu);
   sn::Workspace& ws = sn::g_ws;
-  for (sn::DevBuf* b : {&ws.wins, &ws.pool, &ws.prefix, &ws.status, &ws.kwork, &ws.ctl, &ws.Z, &ws.zr, &ws.sub,
+  for (sn::DevBuf* b : {&ws.wins, &ws.pool, &ws.prefix, &ws.status, &ws.kwork, &ws.ctl, &ws.recs, &ws.Z, &ws.zr, &ws.sub,
                         &ws.bad, &ws.hS, &ws.hQ}) {
     if (b->p) cudaFree(b->p);
     b->p = nullptr;

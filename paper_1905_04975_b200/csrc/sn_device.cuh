@@ -44,13 +44,27 @@ struct StripDev {
 // Per-call device control block.
 struct Control {
   int32_t abort;            // set by a window kernel that rejected a swap
-  int32_t rej_window;       // sorted index of the rejecting window
-  int32_t rej_swaps_done;   // swaps completed in that window before the rejected one
-  int32_t rej_row;          // global first row of the rejected swap
+  int32_t abort_level;      // 1 + DAG level of the rejecting window(s) (claimed by atomicCAS):
+                            // windows of later levels are skipped, every window of that level
+                            // runs (levels are row-disjoint), so the outcome does not depend on
+                            // CTA scheduling
+  int32_t rej_window;       // sorted index of the rejecting window (pencil path)
+  int32_t rej_swaps_done;   // swaps completed in that window before the rejected one (pencil)
+  int32_t rej_row;          // global first row of the rejected swap (pencil path)
   int32_t rej_n1, rej_n2;
   int32_t pad[2];
-  uint8_t rej_sz[256];      // block list of the rejecting window after its last good swap
-  uint8_t rej_sel[256];
+};
+
+// Per-window rejection record (standard path): a window that rejects a swap stores the number
+// of swaps it completed, the rejected pair and its block list after the last good swap here,
+// indexed by its sorted index; several windows of one level may reject.  Zero-initialised,
+// written only by the owning CTA (the sharded executor combines ranks with a max all-reduce).
+struct WinRec {
+  int32_t done;             // swaps completed before the rejection
+  int32_t row;              // global first row of the rejected swap
+  int32_t n1, n2;           // its block sizes
+  uint8_t sz[256];          // block list of [top, top + nblk) after the last good swap
+  uint8_t sel[256];
 };
 
 // status[] of a window: 0 not executed, 1 complete, 2 partial (rejected inside; Z valid)
@@ -67,6 +81,8 @@ struct WindowArgs {
   int16_t* zrange;          // per slot: nonzero row interval of every Z column
   int32_t* status;          // indexed by sorted index
   Control* ctl;
+  WinRec* recs;             // per sorted index: rejection records
+  int32_t level;            // DAG level of this launch
   unsigned long long* tprof;  // debug: per-phase cycle counters (NULL: off)
   int32_t* kwork;           // per sorted index: k4 steps the panel kernels execute per strip,
                             // summed over the 32-row groups of Z^T (Z-structure skipping)
@@ -101,6 +117,14 @@ struct PanelArgs {
   const int16_t* zrange;    // per slot row intervals of Z's columns (window kernel output)
   const PanelMaps* maps;    // host pointer: TMA descriptors (NULL or !valid: cp.async kernel)
 };
+
+// per-device launch state (function attributes are set once per device)
+constexpr int kMaxDevices = 64;
+inline int device_slot() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < kMaxDevices ? d : kMaxDevices - 1;
+}
 
 // kernel launchers (sn_kernels_*.cu)
 void launch_scan(const double* S, int64_t ldS, int64_t n, int32_t validate_lower, uint8_t* subflag,

@@ -128,7 +128,7 @@ struct DBuf {
 };
 
 struct DistWorkspace {
-  DBuf wins, pool, status, ctl, Z, zr, sub, bad;
+  DBuf wins, pool, status, ctl, recs, Z, zr, sub, bad;
   std::vector<DBuf> Sx, own, strips, spref, stage;   // per local rank
   cudaStream_t sB = nullptr, sC = nullptr, sH = nullptr;   // Q / remaining strips / critical path
   cudaEvent_t evW[kZgenD] = {}, evQ[kZgenD] = {}, evCrit[kZgenD] = {}, evRest[kZgenD] = {};
@@ -142,6 +142,22 @@ int ensure_dist_runtime(DistWorkspace& ws, int64_t nlocal) {
   int dev = 0;
   DCK(cudaGetDevice(&dev));
   if (ws.device != dev) {
+    if (ws.device >= 0) {
+      // everything below belongs to the previous device: release it there
+      DCK(cudaSetDevice(ws.device));
+      for (DBuf* b : {&ws.wins, &ws.pool, &ws.status, &ws.ctl, &ws.recs, &ws.Z, &ws.zr, &ws.sub, &ws.bad}) b->release();
+      for (auto* v : {&ws.Sx, &ws.own, &ws.strips, &ws.spref, &ws.stage})
+        for (DBuf& b : *v) b.release();
+      cudaStreamDestroy(ws.sH);
+      cudaStreamDestroy(ws.sB);
+      cudaStreamDestroy(ws.sC);
+      for (int i = 0; i < kZgenD; ++i) {
+        cudaEventDestroy(ws.evW[i]); cudaEventDestroy(ws.evQ[i]);
+        cudaEventDestroy(ws.evCrit[i]); cudaEventDestroy(ws.evRest[i]);
+      }
+      for (cudaEvent_t e : {ws.evIn, ws.evOut, ws.evJoinC, ws.ev0, ws.ev1, ws.evJoin}) cudaEventDestroy(e);
+      DCK(cudaSetDevice(dev));
+    }
     int least = 0, greatest = 0;
     DCK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     DCK(cudaStreamCreateWithPriority(&ws.sH, cudaStreamNonBlocking, greatest));
@@ -268,6 +284,11 @@ int run_dist(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, cons
   DCK(cudaEventRecord(ws.evIn, sUser));
   DCK(cudaStreamWaitEvent(ws.sH, ws.evIn, 0));
   const int rc = run_dist_on(o, n, bc, P, nccl, io, ldu, ldq, select, m, bmap_out, st, ws.sH);
+  // join the Q and remaining-strip streams on every exit path (see sn_abi.cu run())
+  cudaEventRecord(ws.evJoin, ws.sB);
+  cudaStreamWaitEvent(ws.sH, ws.evJoin, 0);
+  cudaEventRecord(ws.evJoinC, ws.sC);
+  cudaStreamWaitEvent(ws.sH, ws.evJoinC, 0);
   cudaEventRecord(ws.evOut, ws.sH);
   cudaStreamWaitEvent(sUser, ws.evOut, 0);
   return rc;
@@ -371,6 +392,7 @@ int run_dist_on(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, c
   DCK(ws.pool.ensure(plan.pool.size() + 8));
   DCK(ws.status.ensure(sizeof(int32_t) * nw));
   DCK(ws.ctl.ensure(sizeof(Control)));
+  DCK(ws.recs.ensure(sizeof(WinRec) * nw));
   const size_t zbytes = sizeof(double) * (size_t)kZslot * (size_t)(kZgenD * maxper);
   if (ws.Z.cap < zbytes) {
     DCK(ws.Z.ensure(zbytes));
@@ -382,6 +404,7 @@ int run_dist_on(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, c
   DCK(cudaMemcpyAsync(ws.pool.p, plan.pool.data(), plan.pool.size(), cudaMemcpyHostToDevice, sA));
   DCK(cudaMemsetAsync(ws.status.p, 0, sizeof(int32_t) * nw, sA));
   DCK(cudaMemsetAsync(ws.ctl.p, 0, sizeof(Control), sA));
+  DCK(cudaMemsetAsync(ws.recs.p, 0, sizeof(WinRec) * nw, sA));
   for (int64_t q = 0; q < nloc; ++q) {
     RankRun& R = rr[q];
     DCK(ws.own[q].ensure(sizeof(WinDev) * std::max<size_t>(1, R.own.size())));
@@ -442,6 +465,7 @@ int run_dist_on(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, c
       wa.wins = R.d_own + a; wa.nwin = (int32_t)c; wa.base = 0;
       wa.pool = (const uint8_t*)ws.pool.p; wa.S = R.Sx; wa.ldS = ldx; wa.Z = dZ;
       wa.status = dstatus; wa.ctl = dctl; wa.zrange = dzr;
+      wa.recs = (WinRec*)ws.recs.p; wa.level = (int32_t)l;
       wa.force_order = o.force_reject_window; wa.force_swap = (int32_t)o.force_reject_swap;
       launch_window(wa, sA);
       launches[0]++;
@@ -457,7 +481,8 @@ int run_dist_on(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, c
         NCK(g_nccl.Broadcast(zr, zr, (size_t)kZrange * 2, ncclUint8, G.wins[i].owner, g_comm.comm, sA));
       }
       NCK(g_nccl.AllReduce(dstatus + w0, dstatus + w0, (size_t)cnt, ncclInt32, ncclMax, g_comm.comm, sA));
-      NCK(g_nccl.AllReduce(&dctl->abort, &dctl->abort, 1, ncclInt32, ncclMax, g_comm.comm, sA));
+      // abort and abort_level (adjacent): every rank skips the levels after a rejection
+      NCK(g_nccl.AllReduce(&dctl->abort, &dctl->abort, 2, ncclInt32, ncclMax, g_comm.comm, sA));
       NCK(g_nccl.GroupEnd());
     }
     if (overlapQ) DCK(cudaEventRecord(ws.evW[gen], sA));
@@ -542,29 +567,26 @@ int run_dist_on(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, c
   DCK(cudaEventElapsedTime(&dev_ms, ws.ev0, ws.ev1));
 
   std::vector<int32_t> status;
+  std::vector<WinRec> recs;
   if (ctl.abort) {
     status.resize(nw);
-    DCK(cudaMemcpy(status.data(), dstatus, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
+    recs.resize(nw);
     if (nccl) {
-      // the rejection record lives on the partial window's owner
-      int root = -1;
-      for (int64_t i = 0; i < nw; ++i)
-        if (status[i] == kWinPartial) root = G.wins[i].owner;
-      if (root >= 0) {
-        NCK(g_nccl.Broadcast(dctl, dctl, sizeof(Control), ncclUint8, root, g_comm.comm, sA));
-        DCK(cudaMemcpyAsync(&ctl, dctl, sizeof(Control), cudaMemcpyDeviceToHost, sA));
-        DCK(cudaStreamSynchronize(sA));
-      }
+      // each partial window's record lives on its owner (the others hold zeros)
+      NCK(g_nccl.AllReduce(ws.recs.p, ws.recs.p, sizeof(WinRec) * nw, ncclUint8, ncclMax, g_comm.comm, sA));
     }
+    DCK(cudaMemcpyAsync(status.data(), dstatus, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost, sA));
+    DCK(cudaMemcpyAsync(recs.data(), ws.recs.p, sizeof(WinRec) * nw, cudaMemcpyDeviceToHost, sA));
+    DCK(cudaStreamSynchronize(sA));
   }
   for (int64_t q = 0; q < nloc; ++q) DCK(copy_blocks(lay, rr[q].rank, rr[q].Sx, ldx, io[q].Su, ldu, false, sA));
   DCK(cudaStreamSynchronize(sA));
 
   // ---- outputs
   std::vector<uint8_t> fsz, fsel;
-  int64_t executed = nw, swaps = 0, sbt[4] = {0, 0, 0, 0};
-  final_blocks(plan, G.sorted, ctl, ctl.abort ? status.data() : nullptr, n, bmap.data(), selrow.data(), fsz, fsel,
-               &executed, &swaps, sbt);
+  int64_t executed = nw, swaps = 0, sbt[4] = {0, 0, 0, 0}, rej = -1;
+  final_blocks(plan, G.sorted, ctl.abort != 0, ctl.abort ? status.data() : nullptr, recs.data(), n, bmap.data(),
+               selrow.data(), fsz, fsel, &executed, &swaps, sbt, &rej);
   write_blocks(fsz, fsel, select, bmap_out);
   if (st) {
     double eqf = 0.0, fk[5] = {0, 0, 0, 0, 0};
@@ -583,11 +605,11 @@ int run_dist_on(const sn_opts& o, int64_t n, int64_t bc, int64_t P, bool nccl, c
     st->inner_windows = plan.ninner;
     st->rejected_window = -1;
     st->rejected_row = -1;
-    if (ctl.abort) {
-      st->rejected_window = plan.wins[G.sorted[ctl.rej_window]].order;
-      st->rejected_row = ctl.rej_row;
-      st->rejected_n1 = ctl.rej_n1;
-      st->rejected_n2 = ctl.rej_n2;
+    if (ctl.abort && rej >= 0) {
+      st->rejected_window = plan.wins[G.sorted[rej]].order;
+      st->rejected_row = recs[rej].row;
+      st->rejected_n1 = recs[rej].n1;
+      st->rejected_n2 = recs[rej].n2;
     }
     st->eq_flops = eqf;
     st->ms_schedule = t_plan - t_start;

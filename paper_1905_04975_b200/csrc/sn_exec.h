@@ -21,10 +21,11 @@ int structure_from_sub(int64_t n, const uint8_t* sub, const int32_t* select, int
                        int64_t* m);
 
 // Final block list after a run: the plan's final list, or, after a rejection, the list of the
-// windows that completed (status per level-sorted window) plus the partial window's list.
-void final_blocks(const Plan& P, const std::vector<int64_t>& sorted, const Control& ctl, const int32_t* status,
-                  int64_t n, const int8_t* bmap, const int8_t* selrow, std::vector<uint8_t>& fsz,
-                  std::vector<uint8_t>& fsel, int64_t* executed, int64_t* swaps, int64_t sbt[4]);
+// windows that completed plus each partial window's own record (recs, by sorted index).
+// rej_sorted: the first partial window in schedule order (sorted index), or -1.
+void final_blocks(const Plan& P, const std::vector<int64_t>& sorted, bool aborted, const int32_t* status,
+                  const WinRec* recs, int64_t n, const int8_t* bmap, const int8_t* selrow, std::vector<uint8_t>& fsz,
+                  std::vector<uint8_t>& fsel, int64_t* executed, int64_t* swaps, int64_t sbt[4], int64_t* rej_sorted);
 
 // select (per-row achieved mask) and bmap_out (may be NULL) from a block list
 void write_blocks(const std::vector<uint8_t>& fsz, const std::vector<uint8_t>& fsel, int32_t* select,

@@ -247,11 +247,12 @@ __global__ void __launch_bounds__(THREADS, 1) panel_kernel(PanelArgs a) {
 template <int MT, int NT, int KIND, int THREADS>
 void launch_t(const PanelArgs& a, int32_t nstrips, cudaStream_t st) {
   using C = Cfg<MT, NT, KIND, THREADS>;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kMaxDevices] = {};   // per device: the attribute is device state
+  const int dslot = device_slot();
+  if (!attr[dslot]) {
     cudaFuncSetAttribute(panel_kernel<MT, NT, KIND, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)C::SMEM);
-    attr = true;
+    attr[dslot] = true;
   }
   panel_kernel<MT, NT, KIND, THREADS><<<nstrips, THREADS, C::SMEM, st>>>(a);
 }

@@ -318,10 +318,11 @@ bool encode_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t oute
 template <int MT, int KIND>
 void launch_tma_t(const PanelArgs& a, int32_t nstrips, const PanelMaps& pm, cudaStream_t st) {
   using C = TCfg<MT>;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kMaxDevices] = {};   // per device: the attribute is device state
+  const int dslot = device_slot();
+  if (!attr[dslot]) {
     cudaFuncSetAttribute(panel_tma_kernel<MT, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    attr = true;
+    attr[dslot] = true;
   }
   int grid = nstrips < 148 ? nstrips : 148;
   const int need = (nstrips + kMaxStripsPerCta - 1) / kMaxStripsPerCta;

@@ -511,9 +511,13 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
   const int widx = blockIdx.x;
   const WinDev wd = a.wins[widx];
   const int sidx = wd.sidx;
-  if (*(volatile int32_t*)&a.ctl->abort) {
-    if (tid == 0) a.status[sidx] = kWinSkipped;
-    return;
+  {
+    // a rejection in an earlier level stops the run; windows of the rejecting level all run
+    const int32_t al = *(volatile int32_t*)&a.ctl->abort_level;
+    if (al != 0 && al - 1 < a.level) {
+      if (tid == 0) a.status[sidx] = kWinSkipped;
+      return;
+    }
   }
   const int k = wd.k, nb = wd.nblk;
   const uint8_t* pool = a.pool + wd.pool;
@@ -558,8 +562,11 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
     }
     __syncthreads();
     if (a.tprof && tid == 0) { const long long c = clock64(); atomicAdd(&a.tprof[6], (unsigned long long)(c - ck)); ck = c; }
-    wavefront_swaps(top, bottom, i1, kin, Din, Zin, recs, W, tid, warp, lane, wd.order == a.force_order,
-                    a.force_swap, swaps_done, a.tprof);
+    // debug knob: reject in the window of schedule order force_order, or (force_order <= -2)
+    // in every window of DAG level -2 - force_order
+    const bool force_here = wd.order == a.force_order || (a.force_order <= -2 && a.level == -2 - a.force_order);
+    wavefront_swaps(top, bottom, i1, kin, Din, Zin, recs, W, tid, warp, lane, force_here, a.force_swap, swaps_done,
+                    a.tprof);
     if (a.tprof && tid == 0) ck = clock64();
     swaps_done = W.done;
     // write the inner window back
@@ -604,13 +611,14 @@ __global__ void __launch_bounds__(kThreads, 1) window_kernel(WindowArgs a) {
   }
   if (tid == 0) {
     if (W.rejected) {
-      a.ctl->abort = 1;
-      a.ctl->rej_window = sidx;
-      a.ctl->rej_swaps_done = swaps_done;
-      a.ctl->rej_row = (int)(j1 + W.rej_row);
-      a.ctl->rej_n1 = W.rej_n1;
-      a.ctl->rej_n2 = W.rej_n2;
-      for (int b = 0; b < nb; ++b) { a.ctl->rej_sz[b] = bsz[b]; a.ctl->rej_sel[b] = bsel[b]; }
+      WinRec* rc = a.recs + sidx;
+      rc->done = swaps_done;
+      rc->row = (int)(j1 + W.rej_row);
+      rc->n1 = W.rej_n1;
+      rc->n2 = W.rej_n2;
+      for (int b = 0; b < nb; ++b) { rc->sz[b] = bsz[b]; rc->sel[b] = bsel[b]; }
+      atomicCAS(&a.ctl->abort_level, 0, a.level + 1);
+      atomicExch(&a.ctl->abort, 1);
       a.status[sidx] = kWinPartial;
     } else {
       a.status[sidx] = kWinDone;
@@ -625,14 +633,18 @@ size_t window_smem_bytes() {
 }
 
 void launch_window(const WindowArgs& a, cudaStream_t st) {
-  static bool attr = false;
-  static int tprof_state = -1;
+  // per device: the opt-in shared-memory attribute and the debug switch are device state
+  static bool attr[kMaxDevices] = {};
+  static int tprof_state[kMaxDevices];
+  static bool init = false;
+  if (!init) { for (int d = 0; d < kMaxDevices; ++d) tprof_state[d] = -1; init = true; }
+  const int dev = device_slot();
   const int want = a.tprof ? 1 : 0;
-  if (tprof_state != want) { cudaMemcpyToSymbol(g_tprof_on, &want, sizeof(int)); tprof_state = want; }
+  if (tprof_state[dev] != want) { cudaMemcpyToSymbol(g_tprof_on, &want, sizeof(int)); tprof_state[dev] = want; }
   const size_t smem = window_smem_bytes();
-  if (!attr) {
+  if (!attr[dev]) {
     cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    attr[dev] = true;
   }
   if (a.nwin > 0) window_kernel<<<a.nwin, kThreads, smem, st>>>(a);
 }

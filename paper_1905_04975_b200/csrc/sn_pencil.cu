@@ -269,7 +269,7 @@ __host__ __device__ __forceinline__ bool pl_std_t22(const double* Tb, double* P,
   return p2r * w0 + p2c * w1 > 0.0;
 }
 
-// The transform of one swap (G1-G4).  A, B: the m x m blocks of S and T (ld 4, m = n1 + n2).
+// The transform of one swap (G1-G4, G7).  A, B: the m x m blocks of S and T (ld 4, m = n1 + n2).
 // Out: U, V (m x m), An = U^T A V, Bn = U^T B V in standard form.  Returns false = rejected.
 template <int N1, int N2>
 __host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double* B, double* U, double* V, double* An,
@@ -304,10 +304,13 @@ __host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double
     else pl_lartg(bx0, bx1, c2, s2, r2);
     U[0] = c2; U[1] = s2; U[4] = -s2; U[5] = c2;
   } else {
-    // G2
+    // G2: Sylvester bases V0, U0, then both re-triangularisations of T's block (xTGEX2): from
+    // the left (U from the QR of (T V0)(:, 1:n2), V = V0) and from the right (V completing the
+    // row space of (U0^T T)(n2+1:m, :), U = U0); keep the one whose S block below the new
+    // leading block is smaller (ties: the left one)
     double R[4] = {0.0, 0.0, 0.0, 0.0}, L[4] = {0.0, 0.0, 0.0, 0.0};
     pl_gsylv<N1, N2>(A, B, R, L);
-    double Mr[16], Ml[16];
+    double Mr[16], Ml[16], U0[16], V0[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) { Mr[i] = 0.0; Ml[i] = 0.0; }
 #pragma unroll
@@ -317,66 +320,52 @@ __host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double
       Mr[(n1 + c) + 4 * c] = 1.0;
       Ml[(n1 + c) + 4 * c] = 1.0;
     }
-    pl_qr_basis(Mr, m, n2, V);
-    pl_qr_basis(Ml, m, n2, U);
+    pl_qr_basis(Mr, m, n2, V0);
+    pl_qr_basis(Ml, m, n2, U0);
+    double I4[16], TV[16], UT[16], Uq[16], H[16], Vr[16], Aq[16], Ar[16];
+    pl_eye(I4, m);
+    pl_congr(I4, B, V0, TV, m);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) { Mr[i] = 0.0; Ml[i] = 0.0; }
+#pragma unroll
+    for (int c = 0; c < n2; ++c)
+#pragma unroll
+      for (int r = 0; r < m; ++r) Ml[r + 4 * c] = TV[r + 4 * c];
+    pl_qr_basis(Ml, m, n2, Uq);
+    pl_congr(U0, B, I4, UT, m);
+#pragma unroll
+    for (int c = 0; c < n1; ++c)
+#pragma unroll
+      for (int r = 0; r < m; ++r) Mr[r + 4 * c] = UT[(n2 + c) + 4 * r];
+    pl_qr_basis(Mr, m, n1, H);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) Vr[i] = 0.0;
+#pragma unroll
+    for (int c = 0; c < n2; ++c)
+#pragma unroll
+      for (int r = 0; r < m; ++r) Vr[r + 4 * c] = H[r + 4 * (n1 + c)];
+#pragma unroll
+    for (int c = 0; c < n1; ++c)
+#pragma unroll
+      for (int r = 0; r < m; ++r) Vr[r + 4 * (n2 + c)] = H[r + 4 * c];
+    pl_congr(Uq, A, V0, Aq, m);
+    pl_congr(U0, A, Vr, Ar, m);
+    const double rq = pl_lowfro(Aq, n1, n2), rr = pl_lowfro(Ar, n1, n2);
+    const bool left = rq <= rr;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) { U[i] = left ? Uq[i] : U0[i]; V[i] = left ? V0[i] : Vr[i]; }
   }
   pl_congr(U, A, V, An, m);
   pl_congr(U, B, V, Bn, m);
-  if (!(n1 == 1 && n2 == 1) && !(pl_lowfro(An, n1, n2) <= thA && pl_lowfro(Bn, n1, n2) <= thB)) {
-      // G2b: re-triangularise T's block from the left (U from the QR of (T V)(:, 1:n2)) or from
-      // the right (V completing the row space of (U^T T)(n2+1:m, :)); keep the variant whose S
-      // block below the new leading block is smaller
-      double I4[16], TV[16], UT[16], Uq[16], H[16], Vr[16], Aq[16], Ar[16];
-      pl_eye(I4, m);
-      pl_congr(I4, B, V, TV, m);
-      pl_congr(U, B, I4, UT, m);
-      double Ml[16], Mr[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) { Mr[i] = 0.0; Ml[i] = 0.0; }
-#pragma unroll
-      for (int c = 0; c < n2; ++c)
-#pragma unroll
-        for (int r = 0; r < m; ++r) Ml[r + 4 * c] = TV[r + 4 * c];
-#pragma unroll
-      for (int c = 0; c < n1; ++c)
-#pragma unroll
-        for (int r = 0; r < m; ++r) Mr[r + 4 * c] = UT[(n2 + c) + 4 * r];
-      pl_qr_basis(Ml, m, n2, Uq);
-      pl_qr_basis(Mr, m, n1, H);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) Vr[i] = 0.0;
-#pragma unroll
-      for (int c = 0; c < n2; ++c)
-#pragma unroll
-        for (int r = 0; r < m; ++r) Vr[r + 4 * c] = H[r + 4 * (n1 + c)];
-#pragma unroll
-      for (int c = 0; c < n1; ++c)
-#pragma unroll
-        for (int r = 0; r < m; ++r) Vr[r + 4 * (n2 + c)] = H[r + 4 * c];
-      pl_congr(Uq, A, V, Aq, m);
-      pl_congr(U, A, Vr, Ar, m);
-      double rq = 0.0, rr = 0.0;
-#pragma unroll
-      for (int c = 0; c < n2; ++c)
-#pragma unroll
-        for (int r = n2; r < m; ++r) { rq = fma(Aq[r + 4 * c], Aq[r + 4 * c], rq); rr = fma(Ar[r + 4 * c], Ar[r + 4 * c], rr); }
-      if (rq <= rr) { for (int i = 0; i < 16; ++i) U[i] = Uq[i]; }
-      else { for (int i = 0; i < 16; ++i) V[i] = Vr[i]; }
-    pl_congr(U, A, V, An, m);
-    pl_congr(U, B, V, Bn, m);
-  }
-  // G3
-  double resA = 0.0, resB = 0.0;
-#pragma unroll
-  for (int c = 0; c < n2; ++c)
-#pragma unroll
-    for (int r = n2; r < m; ++r) {
-      resA = fma(An[r + 4 * c], An[r + 4 * c], resA);
-      resB = fma(Bn[r + 4 * c], Bn[r + 4 * c], resB);
+  // G3 (xTGEX2's weak test): 1x1|1x1 both blocks below the new leading block; otherwise S's
+  // (T's is zero by the re-triangularisation)
+  {
+    const double resA = pl_lowfro(An, n1, n2), resB = pl_lowfro(Bn, n1, n2);
+    const bool pass = (n1 == 1 && n2 == 1) ? (resA <= thA && resB <= thB) : (resA <= thA);
+    if (!pass) {
+      if (why) { why[0] = 1.0; why[1] = (n1 == 1 && n2 == 1) ? fmax(resA / thA, resB / thB) : resA / thA; }
+      return false;
     }
-  if (!(sqrt(resA) <= thA && sqrt(resB) <= thB)) {
-    if (why) { why[0] = 1.0; why[1] = fmax(sqrt(resA) / thA, sqrt(resB) / thB); }
-    return false;
   }
 #pragma unroll
   for (int c = 0; c < n2; ++c)
@@ -430,6 +419,30 @@ __host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double
 #pragma unroll
     for (int r = 0; r < m; ++r) U[r + 4 * p] = -U[r + 4 * p];
   }
+  // G7: the largest-magnitude entry (the first such) of every column of V is positive; U's
+  // column follows, the blocks change as D An D, D Bn D
+  double d[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    int im = 0;
+#pragma unroll
+    for (int r = 1; r < m; ++r)
+      if (fabs(V[r + 4 * c]) > fabs(V[im + 4 * c])) im = r;
+    double vm = V[4 * c];
+#pragma unroll
+    for (int r = 1; r < m; ++r)
+      if (r == im) vm = V[r + 4 * c];
+    d[c] = (c < m && vm < 0.0) ? -1.0 : 1.0;
+  }
+#pragma unroll
+  for (int c = 0; c < m; ++c)
+#pragma unroll
+    for (int r = 0; r < m; ++r) {
+      U[r + 4 * c] *= d[c];
+      V[r + 4 * c] *= d[c];
+      An[r + 4 * c] *= d[r] * d[c];
+      Bn[r + 4 * c] *= d[r] * d[c];
+    }
   return true;
 }
 

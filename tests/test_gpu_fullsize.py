@@ -8,8 +8,8 @@ properties that hold at any size (north_star invariants):
   * 1x1 eigenvalues bitwise equal along the permutation, 2x2 eigenvalues within 1e-10 relative;
   * sketched residual ||(A - Q S Q^T) X|| / ||A X|| and orthogonality ||(Q^T Q - I) X|| / ||X||
     with a Gaussian X of 16 columns (harness arithmetic: torch FP64 matmul), <= 100 n eps;
-plus, for config 3, prefix parity with the oracle (the first 2 windows on both sides, all of
-S and Q compared elementwise within 1e-9 ||S||_F).
+plus, for config 3, prefix parity with the oracle (the first 32 windows on both sides, >= 3 DAG
+levels, all of S and Q compared elementwise within 1e-9 ||S||_F).
 """
 import numpy as np
 import pytest
@@ -58,7 +58,7 @@ def _entries(T, rows, cols):
     return T[torch.as_tensor(cols, device=T.device), torch.as_tensor(rows, device=T.device)].cpu().numpy()
 
 
-def _run_fullsize(cfg, prefix_windows=0):
+def _run_fullsize(cfg, prefix_windows=0, min_levels=1):
     p = make_config(cfg, seed=1, device="cuda")
     n = p.n
     S, Q = p.S, p.Q                      # row-major tensors holding S^T, Q^T
@@ -82,6 +82,8 @@ def _run_fullsize(cfg, prefix_windows=0):
         Sp, Qp = S.clone(), Q.clone()
         got = sn.reorder(Sp, Qp, p.select, window=p.w, max_windows=prefix_windows)
         torch.cuda.synchronize()
+        # the prefix must exercise the multi-level executor (lookahead strips, Q overlap)
+        assert got["stats"]["levels"] >= min_levels, got["stats"]["levels"]
         ref = oracle.reorder(S0h, Q0h, p.select, w=p.w, mode=1, max_windows=prefix_windows, inplace=True)
         assert got["rc"] == 0 == ref["rc"]
         np.testing.assert_array_equal(got["bmap"], ref["bmap"])
@@ -133,8 +135,37 @@ def _run_fullsize(cfg, prefix_windows=0):
 
 
 def test_config3_fullsize_bench_launch():
-    _run_fullsize(3, prefix_windows=2)
+    # 32 windows of the schedule spanning several DAG levels, in the bench launch
+    # configuration (lookahead and Q-stream overlap on), compared over all of S and Q
+    _run_fullsize(3, prefix_windows=32, min_levels=3)
 
 
 def test_config4_fullsize_worst_case_chain():
     _run_fullsize(4)
+
+
+def test_config4_prefix_parity_sampled_Q():
+    """Config 4 (n = 65 536, worst-case chain): the first 16 windows against the oracle, all of
+    S and a 4 096-row sample of Q (or_reorder_q: Q's rows are updated independently; the full
+    Q does not fit twice in host memory beside S), elementwise within 1e-9 ||S||_F."""
+    p = make_config(4, seed=1, device="cuda")
+    n, K = p.n, 16
+    S, Q = p.S, p.Q
+    rows = np.sort(np.random.default_rng(3).choice(n, 4096, replace=False))
+    S0h = np.asfortranarray(S.cpu().numpy().T)                       # no copy: S^T row-major
+    Q0s = np.asfortranarray(Q[:, torch.as_tensor(rows, device="cuda")].cpu().numpy().T)
+    nS = float(torch.linalg.norm(S).item())
+    got = sn.reorder(S, Q, p.select, window=p.w, max_windows=K)
+    torch.cuda.synchronize()
+    assert got["rc"] == 0 and got["stats"]["windows"] == K
+    ref = oracle.reorder(S0h, Q0s, p.select, w=p.w, mode=1, max_windows=K, inplace=True)
+    assert ref["rc"] == 0 and ref["stats"]["windows"] == K
+    np.testing.assert_array_equal(got["bmap"], ref["bmap"])
+    dS = 0.0
+    for c0 in range(0, n, 4096):                                       # column blocks of S
+        blk = S[c0:c0 + 4096].cpu().numpy()                            # = S[:, c0:c0+4096]^T
+        dS = max(dS, float(np.abs(blk - ref["S"][:, c0:c0 + 4096].T).max()))
+    dQ = float(np.abs(Q[:, torch.as_tensor(rows, device="cuda")].cpu().numpy().T - ref["Q"]).max())
+    print("config4 prefix K=%d levels=%d: max|dS|/||S||=%.3g max|dQ| (4096 rows)=%.3g"
+          % (K, got["stats"]["levels"], dS / nS, dQ))
+    assert dS <= 1e-9 * nS and dQ <= 1e-9 * nS

@@ -3,10 +3,10 @@
 The CUDA path (sn_reorder_pencil_ex: the window kernel with the pencil swap and the TMA panel
 kernels on S, T, Q, Z) against the oracle's windowed generalized reordering (or_greorder mode
 1, pinned to LAPACK dtgexc / dtgsen in tests/test_oracle_generalized.py) on the same seeded
-pencils: block map and selection bit-exact, S, T, Q, Z within 1e-9 ||.||_F elementwise up to
-the signs of the basis vectors (the in-window swap order differs, reading R12, so agreement is
-to rounding, and a rounding-level decision may flip a basis vector's sign convention), and the
-invariants of a generalized reordering.
+pencils: block map and selection bit-exact, S, T, Q, Z elementwise within 1e-9 ||S||_F (the
+in-window swap order differs, reading R12, so agreement is to rounding; the basis-sign
+convention G7 makes the signs a function of the data, not of rounding-level choices such as
+which re-triangularisation G2 keeps), and the invariants of a generalized reordering.
 """
 import numpy as np
 import pytest
@@ -14,6 +14,7 @@ import torch
 
 import oracle
 import paper_1905_04975_b200 as sn
+from tests.helpers import blocks_of, bmap_from_S, stable_partition
 from tests.test_oracle_generalized import check_greordering, check_gstructure
 from workloads import make_pencil
 
@@ -54,23 +55,13 @@ def _compare(p, window, **kw):
     np.testing.assert_array_equal(r["bmap"], ref["bmap"])
     np.testing.assert_array_equal(r["select"], ref["select"])
     nS, nT = np.linalg.norm(S), np.linalg.norm(T)
-    if r["Q"] is not None and r["Z"] is not None:
-        # the sign of each basis vector (each column of Q and of Z) is a convention that a
-        # rounding-level decision can flip (G2b on a borderline residual, a near-tie in the
-        # 2x2 SVD): compare Ŝ, T̂ up to these diagonal sign matrices, exactly as determined
-        # by Q and Z, and Q, Z column by column up to sign
-        dQ = np.where(np.einsum("ij,ij->j", r["Q"], ref["Q"]) < 0, -1.0, 1.0)
-        dZ = np.where(np.einsum("ij,ij->j", r["Z"], ref["Z"]) < 0, -1.0, 1.0)
-        assert np.abs(r["S"] - dQ[:, None] * ref["S"] * dZ[None, :]).max() <= 1e-9 * nS
-        assert np.abs(r["T"] - dQ[:, None] * ref["T"] * dZ[None, :]).max() <= 1e-9 * nT
-        assert np.abs(r["Q"] - ref["Q"] * dQ[None, :]).max() <= 1e-9 * max(nS, 1.0)
-        assert np.abs(r["Z"] - ref["Z"] * dZ[None, :]).max() <= 1e-9 * max(nS, 1.0)
-    else:
-        assert np.abs(np.abs(r["S"]) - np.abs(ref["S"])).max() <= 1e-9 * nS
-        assert np.abs(np.abs(r["T"]) - np.abs(ref["T"])).max() <= 1e-9 * nT
-        for key in ("Q", "Z"):
-            if r[key] is not None:
-                assert np.abs(np.abs(r[key]) - np.abs(ref[key])).max() <= 1e-9 * max(nS, 1.0)
+    worst = 0.0
+    for key, nrm in (("S", nS), ("T", nT), ("Q", max(nS, 1.0)), ("Z", max(nS, 1.0))):
+        if r[key] is not None:
+            d = np.abs(r[key] - ref[key]).max() / nrm
+            worst = max(worst, d)
+            assert d <= 1e-9, (key, d)
+    print("pencil n=%d: max elementwise diff / norm = %.3g" % (S.shape[0], worst))
     if Q is not None and Z is not None:
         check_greordering(S, T, Q, Z, p.select, r)
     else:
@@ -160,3 +151,58 @@ def test_pencil_identity_T_matches_standard_path():
         return q @ q.T
     assert np.abs(proj(_host(dQ)[:, :m]) - proj(_host(dQ2)[:, :m])).max() <= 1e-10
     assert np.abs(_host(dT) - np.eye(300)).max() <= 1e-12
+
+
+def _gpu_invariants(S0, T0, Q0, Z0, dS, dT, dQ, dZ, tol):
+    """Residual and orthogonality with FP64 torch matmuls on the device (harness arithmetic;
+    the dense CPU check is too slow at n = 16 384)."""
+    n = S0.shape[0]
+    I = torch.eye(n, dtype=torch.float64, device="cuda")
+    Qd, Zd = dQ.t(), dZ.t()                          # the tensors hold X^T
+    Q0d, Z0d = torch.as_tensor(Q0).cuda(), torch.as_tensor(Z0).cuda()
+    for X0, dX in ((S0, dS), (T0, dT)):
+        A = Q0d @ torch.as_tensor(X0).cuda() @ Z0d.t()
+        res = (torch.linalg.norm(A - Qd @ dX.t() @ Zd.t()) / torch.linalg.norm(A)).item()
+        assert res <= tol, res
+    for M in (Qd, Zd):
+        assert torch.linalg.norm(M.t() @ M - I).item() <= tol
+
+
+def test_pencil_config2_size_completes_with_prefix_parity():
+    """a config-2-shaped pencil (n = 16 384, w = 256, 25 % 2x2 blocks,
+    Bernoulli(0.35)) -- rejected at window 1 645 by the previous swap -- completes (rc 0) with
+    the xTGEX2 two-variant re-triangularisation (G2); the first 16 windows (several DAG
+    levels) match the oracle elementwise; the whole run meets the invariants."""
+    p = make_pencil(16384, p2=0.25, q="householder", psel=0.35, w=256, seed=1)
+    S, T, Q, Z = p.np("S"), p.np("T"), p.np("Q"), p.np("Z")
+    K = 16
+    dS, dT, dQ, dZ = _dev(S), _dev(T), _dev(Q), _dev(Z)
+    r = sn.reorder_pencil(dS, dT, dQ, dZ, p.select, window=256, max_windows=K)
+    torch.cuda.synchronize()
+    ref = oracle.greorder(S, T, Q, Z, p.select, w=256, mode=1, max_windows=K)
+    assert r["rc"] == 0 == ref["rc"] and r["stats"]["windows"] == K == ref["stats"]["windows"]
+    np.testing.assert_array_equal(r["bmap"], ref["bmap"])
+    nS = np.linalg.norm(S)
+    worst = 0.0
+    for key, d in (("S", dS), ("T", dT), ("Q", dQ), ("Z", dZ)):
+        worst = max(worst, np.abs(_host(d) - ref[key]).max() / nS)
+    print("pencil n=16384 prefix K=%d levels=%d: max diff / ||S||_F = %.3g" % (K, r["stats"]["levels"], worst))
+    assert worst <= 1e-9
+    assert r["stats"]["levels"] >= 3
+    del ref
+    # the whole reordering
+    dS, dT, dQ, dZ = _dev(S), _dev(T), _dev(Q), _dev(Z)
+    r = sn.reorder_pencil(dS, dT, dQ, dZ, p.select, window=256)
+    torch.cuda.synchronize()
+    print("pencil n=16384 full: rc=%d windows=%d levels=%d swaps=%d ms_device=%.1f"
+          % (r["rc"], r["stats"]["windows"], r["stats"]["levels"], r["stats"]["swaps"], r["stats"]["ms_device"]))
+    assert r["rc"] == 0
+    n = S.shape[0]
+    b0 = blocks_of(bmap_from_S(S))
+    flags = np.array([bool(p.select[q] or (sz == 2 and p.select[q + 1])) for q, sz in b0])
+    sizes = np.array([sz for _, sz in b0])
+    order = stable_partition(sizes, flags)
+    exp_bmap = np.concatenate([[0] if sizes[t] == 1 else [1, 2] for t in order]).astype(np.int8)
+    np.testing.assert_array_equal(r["bmap"], exp_bmap)
+    np.testing.assert_array_equal(check_gstructure(_host(dS), _host(dT)), exp_bmap)
+    _gpu_invariants(S, T, Q, Z, dS, dT, dQ, dZ, 100 * n * np.finfo(float).eps)

@@ -411,3 +411,101 @@ def test_forced_rejection_leaves_consistent_state(mode):
     assert int(r["select"].sum()) == r["m"]
     # the selected 1x1 eigenvalues are still present in the reported selected rows
     assert r["select"][r["stats"]["rejected_row"] + r["stats"]["rejected_n1"]] == 1
+
+
+# ---- natural rejections: the weak test (c4 #5) and the 2x2 split (R6)
+def _near_pair(rng, n1, n2):
+    """Adjacent blocks with nearly equal eigenvalues (pairs lam +- i mu, mu in [1e-9, 1e-3])
+    and a coupling up to 1e8: ill-conditioned Sylvester equations, where LAPACK dtrexc
+    rejects (info = 1) or splits a moved 2x2 block into two real eigenvalues."""
+    lam, mu, big = rng.uniform(-1, 1), 10 ** rng.uniform(-9, -3), 10 ** rng.uniform(0, 8)
+
+    def blk2(l, m):
+        b = rng.uniform(0.5, 2)
+        return np.array([[l, b], [-m * m / b, l]])
+    n = n1 + n2
+    T = np.zeros((n, n))
+    near = lambda: lam + rng.uniform(-1, 1) * mu  # noqa: E731
+    if n1 == 1:
+        T[0, 0] = near()
+    else:
+        T[:2, :2] = blk2(lam, mu)
+    if n2 == 1:
+        T[n1, n1] = near()
+    else:
+        T[n1:, n1:] = blk2(near(), mu * rng.uniform(0.5, 2))
+    T[:n1, n1:] = rng.standard_normal((n1, n2)) * big
+    return np.asfortranarray(T)
+
+
+@pytest.mark.parametrize("n1,n2", [(2, 1), (2, 2)])
+def test_natural_rejections_match_dtrexc(n1, n2):
+    """Without any forcing: where LAPACK dtrexc rejects the swap (info = 1) the oracle's weak
+    test rejects it (reason 1); where dtrexc splits a moved 2x2 block, the oracle rejects by
+    reading R6 (reason 2); where dtrexc swaps normally, the oracle swaps.  Rejected swaps leave
+    T and Q bitwise untouched."""
+    rng = np.random.default_rng(5 + 10 * n1 + n2)
+    n = n1 + n2
+    tab = {}
+    for _ in range(1500):
+        T = _near_pair(rng, n1, n2)
+        Tl, _, info = lapack.dtrexc(T.copy(), np.eye(n), n1 + 1, 1)
+        exp = [False] * (n - 1)
+        if n2 == 2:
+            exp[0] = True
+        if n1 == 2:
+            exp[n2] = True
+        split = [bool(Tl[i + 1, i] != 0) for i in range(n - 1)] != exp
+        lap = 1 if info else (2 if split else 0)
+        rc, T1, Q1 = oracle.swap(T, 0, n1, n2, np.eye(n, order="F"))
+        why = oracle.swap_last_reject()
+        assert rc == (1 if why else 0)
+        if rc:
+            assert np.array_equal(T1, T) and np.array_equal(Q1, np.eye(n))
+        tab[(lap, why)] = tab.get((lap, why), 0) + 1
+    agree = sum(v for (a, b), v in tab.items() if a == b)
+    print((n1, n2), tab)
+    assert agree >= 0.99 * 1500, tab
+    assert tab.get((2, 2), 0) >= 100                       # the split branch fires
+    if n1 == 2 and n2 == 2:
+        assert tab.get((1, 1), 0) >= 100                   # the weak test fires
+
+
+def test_natural_rejection_in_reordering_matches_dtrsen():
+    """A whole reordering that must pass an ill-conditioned 2x2|2x2 pair: LAPACK dtrsen
+    fails (info = 1) and so does the oracle (rc = 1, both modes), leaving a valid partially
+    reordered form and reporting the pair."""
+    rng = np.random.default_rng(77)
+    for _ in range(200):
+        B = _near_pair(rng, 2, 2)
+        if lapack.dtrexc(B.copy(), np.eye(4), 3, 1)[2] == 1:
+            break
+    n = 7
+    S = np.triu(rng.standard_normal((n, n)))
+    S[0, 0], S[1, 1], S[2, 2] = 4.0, -3.0, 6.5
+    S[3:, 3:] = B
+    S = np.asfortranarray(S)
+    Q = np.asfortranarray(np.linalg.qr(rng.standard_normal((n, n)))[0])
+    sel = np.zeros(n, np.int32)
+    sel[5] = sel[6] = 1                                    # the lower 2x2 block must pass the upper
+    *_, info = lapack.dtrsen(sel, S.copy(), Q.copy(), job="N")
+    assert info == 1
+    for mode in (0, 1):
+        r = oracle.reorder(S, Q, sel, w=8, mode=mode)
+        assert r["rc"] == 1 and r["stats"]["rejected_row"] == 3 and r["stats"]["rejected_n1"] == 2
+        A = Q @ S @ Q.T
+        assert np.linalg.norm(A - r["Q"] @ r["S"] @ r["Q"].T) / np.linalg.norm(A) <= 100 * n * EPS
+        np.testing.assert_array_equal(r["bmap"], bmap_from_S(r["S"]))
+        assert r["select"][5:7].sum() == 2 and r["m"] == 2   # the block stopped below the pair
+
+
+def test_row_sampled_Q_gives_those_rows():
+    """or_reorder_q: a row sample of Q yields exactly those rows of the full result (the
+    rows of Q <- Q Q3 are independent), used for prefix parity at config 4."""
+    p = make_problem(300, p2=0.25, q="householder", psel=0.4, w=32, seed=3)
+    S0, Q0 = p.S_np().copy(order="F"), p.Q_np().copy(order="F")
+    rows = np.array([0, 5, 77, 150, 299])
+    for mode in (0, 1):
+        a = oracle.reorder(S0, Q0, p.select, w=32, mode=mode)
+        b = oracle.reorder(S0, np.asfortranarray(Q0[rows]), p.select, w=32, mode=mode)
+        assert np.array_equal(a["S"], b["S"]) and np.array_equal(a["Q"][rows], b["Q"])
