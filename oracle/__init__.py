@@ -77,6 +77,8 @@ def lib():
         _lib.or_eig_count.restype = i32
         _lib.or_eigvec.argtypes = [i64, p, i64, p, i64, p, p, i64, p]
         _lib.or_eigvec.restype = i32
+        _lib.or_qr_sweep.argtypes = [i64, p, i64, p, i64, i64, i64, p, p]
+        _lib.or_qr_sweep.restype = i32
         _lib.or_greorder.argtypes = [i32, i64, p, i64, p, i64, p, i64, p, i64, p, C.POINTER(C.c_int64),
                                      i64, i64, i64, p, C.POINTER(Stats)]
         _lib.or_greorder.restype = i32
@@ -281,3 +283,21 @@ def eigvec(S, Q, select_rows):
     e = np.zeros(max(nc.value, 1), np.int32)
     rc = lib().or_eigvec(n, _ptr(Sx), max(n, 1), _ptr(Qx), max(n, 1), _ptr(sel), _ptr(X), max(n, 1), _ptr(e))
     return rc, X, e[:nc.value]
+
+
+# ---- bulge-chasing sweep (sn_oracle.h) ----------------------------------
+
+def qr_sweep(H, Q, sr, si, inplace: bool = False):
+    """One multishift QR sweep (readings B1-B5) on the Hessenberg H with the shifts sr + i si;
+    Q (n x n, or a row sample nq x n) accumulates.  Returns (rc, H', Q')."""
+    if inplace:
+        Hx, Qx = H, Q
+    else:
+        Hx = _f64(H).copy(order="F")
+        Qx = None if Q is None else _f64(Q).copy(order="F")
+    n = Hx.shape[0]
+    nq = n if Qx is None else Qx.shape[0]
+    sr = np.ascontiguousarray(sr, np.float64)
+    si = np.ascontiguousarray(si, np.float64)
+    rc = lib().or_qr_sweep(n, _ptr(Hx), max(n, 1), _ptr(Qx), max(nq, 1), nq, len(sr), _ptr(sr), _ptr(si))
+    return rc, Hx, Qx

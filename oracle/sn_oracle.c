@@ -1384,10 +1384,10 @@ int or_greorder(int mode, int64_t n, double* S, int64_t lds, double* T, int64_t 
  * ========================================================================= */
 #define OR_OMEGA 3.273390607896142e+150   /* 2^500 */
 
-/* smallest s >= 0 with v * 2^-s <= lim (v, lim > 0) */
+/* smallest s >= 0 with v * 2^-s <= lim (v, lim > 0; v finite) */
 static int pow2_steps(double v, double lim) {
   int s = 0;
-  while (v > lim) { v *= 0.5; ++s; }
+  while (v > lim && s < 4000) { v *= 0.5; ++s; }
   return s;
 }
 
@@ -1506,7 +1506,20 @@ int or_eigvec(int64_t n, const double* S, int64_t lds, const double* Q, int64_t 
     }
     const double smin = dmax(eps * (fabs(wr) + fabs(wi)), smlnum);
     int e = 0;                                     /* the column holds (true vector) * 2^-e */
-    /* right-hand side of the rows above: r_l = -S[l, k:k+bs] y_blk */
+    /* right-hand side of the rows above: r_l = -S[l, k:k+bs] y_blk (protected as E4) */
+    {
+      double cmax = 0.0, ymax = 0.0;
+      for (int64_t l = 0; l < k; ++l)
+        for (int q = 0; q < bs; ++q) cmax = dmax(cmax, fabs(IDX(S, lds, l, k + q)));
+      for (int q = 0; q < bs; ++q) ymax = dmax(ymax, cabs1(yr[k + q], yi[k + q]));
+      const double g = ((double)bs * (ymax / OR_OMEGA)) * cmax;   /* (growth) / Omega */
+      if (g > 1.0) {
+        const int s = pow2_steps(g, 1.0);
+        const double f = ldexp(1.0, -s);
+        for (int q = 0; q < bs; ++q) { yr[k + q] *= f; yi[k + q] *= f; }
+        e += s;
+      }
+    }
     for (int64_t l = 0; l < k; ++l)
       for (int q = 0; q < bs; ++q) {
         yr[l] -= IDX(S, lds, l, k + q) * yr[k + q];
@@ -1529,13 +1542,13 @@ int or_eigvec(int64_t n, const double* S, int64_t lds, const double* Q, int64_t 
          * scaled and the small system solved again: exact powers of two) */
         double rmax = dmax(cabs1(rr[0], ri[0]), nb == 2 ? cabs1(rr[1], ri[1]) : 0.0);
         int s = 1;
-        if (ymax == ymax && ymax < 1e308) s = pow2_steps(ymax, OR_OMEGA);
-        else s = pow2_steps(rmax, OR_OMEGA * smin) + 1;
+        if (ymax < 1e308) s = pow2_steps(ymax, OR_OMEGA);
+        else s = pow2_steps(rmax / smin, OR_OMEGA) + 1;   /* |y| <~ |r| / smin */
         for (;;) {
           const double f = ldexp(1.0, -s);
           double r2r[2] = {rr[0] * f, rr[1] * f}, r2i[2] = {ri[0] * f, ri[1] * f};
           ymax = small_csolve(nb, B, wr, wi, smin, r2r, r2i, sr, si);
-          if (ymax <= OR_OMEGA) break;
+          if (ymax <= OR_OMEGA || s > 4000) break;
           ++s;
         }
         const double f = ldexp(1.0, -s);
@@ -1550,9 +1563,9 @@ int or_eigvec(int64_t n, const double* S, int64_t lds, const double* Q, int64_t 
         rmax = dmax(rmax, cabs1(yr[l], yi[l]));
         for (int q = 0; q < nb; ++q) cmax = dmax(cmax, fabs(IDX(S, lds, l, i + q)));
       }
-      const double grow = rmax + (double)nb * cmax * ymax;
-      if (grow > OR_OMEGA) {
-        const int s = pow2_steps(grow, OR_OMEGA);
+      const double g = rmax / OR_OMEGA + ((double)nb * (ymax / OR_OMEGA)) * cmax;   /* (growth) / Omega */
+      if (g > 1.0) {
+        const int s = pow2_steps(g, 1.0);
         const double f = ldexp(1.0, -s);
         for (int64_t l = 0; l < n; ++l) { yr[l] *= f; yi[l] *= f; }
         e += s;
@@ -1591,5 +1604,113 @@ int or_eigvec(int64_t n, const double* S, int64_t lds, const double* Q, int64_t 
     k += bs;
   }
   free(yr); free(yi); free(bmap);
+  return 0;
+}
+
+/* ===========================================================================
+ * Bulge-chasing sweep of the multishift QR algorithm.  PAPER.md
+ * "The bulge chasing step creates a set of bulges which are chased
+ * down the diagonal to complete one pipelined QR iteration.  This is
+ * accomplished by applying sequences of overlapping 3 x 3 Householder
+ * reflectors to H."  Readings B1-B5:
+ *   B1  shifts come in pairs (s_2j, s_2j+1): two real shifts or a complex
+ *       conjugate pair; pair j makes bulge j (a double-shift Francis step).
+ *   B2  bulge j is introduced at the top by the reflector that maps
+ *       p_j(H) e1 = (H^2 - sigma H + pi I) e1 (rows 0..2; sigma = s + s',
+ *       pi = s s') onto e1 (Golub & Van Loan, Algorithm 7.5.1).
+ *   B3  chase: for p = 1 .. n-3 the reflector from H[p:p+3, p-1] (3 entries)
+ *       annihilates H[p+1, p-1], H[p+2, p-1]; for p = n-2 a 2-element
+ *       reflector from H[n-2:n, n-3].  Each reflector is applied from the
+ *       left to its rows (columns p-1 .. n-1), from the right to its columns
+ *       (rows 0 .. min(p+3, n-1)) and to the columns of Q; the annihilated
+ *       entries are set to exact zeros.  Reflectors follow xLARFG (R3).
+ *   B4  one sweep = bulge 0 chased to the bottom, then bulge 1, ...: in exact
+ *       arithmetic the same reflectors as the pipelined chain of bulges the
+ *       paper describes (bulges spaced >= 4 rows apart; each reflector reads
+ *       only entries every earlier bulge has finished with), so the windowed
+ *       GPU chase agrees with it to rounding.
+ *   B5  Q may hold nq <= n rows (row sample, as or_reorder_q).
+ * ========================================================================= */
+static void or_larfg2(double* alpha, double* x, double* tau) {
+  /* 2-element xLARFG: H (alpha, x) = (beta, 0), v = (1, x'), beta = -sign(alpha) ||.|| */
+  if (*x == 0.0) { *tau = 0.0; return; }
+  const double beta = -copysign(lapy2(*alpha, *x), *alpha);
+  *tau = (beta - *alpha) / beta;
+  *x = *x / (*alpha - beta);
+  *alpha = beta;
+}
+
+/* apply H = I - tau v v^T (v of length m, v[0] = 1) to rows r0..r0+m-1, columns c0..c1-1 */
+static void refl_left_m(double* A, int64_t lda, int m, int64_t r0, int64_t c0, int64_t c1, const double* v,
+                        double tau) {
+  if (tau == 0.0) return;
+  for (int64_t c = c0; c < c1; ++c) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += v[i] * IDX(A, lda, r0 + i, c);
+    s *= tau;
+    for (int i = 0; i < m; ++i) IDX(A, lda, r0 + i, c) -= s * v[i];
+  }
+}
+
+/* apply H from the right to columns c0..c0+m-1, rows r0..r1-1 */
+static void refl_right_m(double* A, int64_t lda, int m, int64_t c0, int64_t r0, int64_t r1, const double* v,
+                         double tau) {
+  if (tau == 0.0) return;
+  for (int64_t r = r0; r < r1; ++r) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += IDX(A, lda, r, c0 + i) * v[i];
+    s *= tau;
+    for (int i = 0; i < m; ++i) IDX(A, lda, r, c0 + i) -= s * v[i];
+  }
+}
+
+int or_qr_sweep(int64_t n, double* H, int64_t ldh, double* Q, int64_t ldq, int64_t nq, int64_t nshift,
+                const double* sr, const double* si) {
+  if (n < 0) return -1;
+  if (n > 0 && (H == NULL || ldh < n)) return -2;
+  if (Q && (nq < 0 || nq > n || ldq < (nq > 1 ? nq : 1))) return -4;
+  if (nshift < 0 || (nshift & 1)) return -7;
+  if (nshift > 0 && (sr == NULL || si == NULL)) return -8;
+  for (int64_t j = 0; j < nshift; j += 2) {
+    const int conj = si[j] != 0.0 || si[j + 1] != 0.0;
+    if (conj && !(sr[j] == sr[j + 1] && si[j] == -si[j + 1])) return -9;   /* B1 */
+  }
+  if (n < 3) return 0;
+  for (int64_t j = 0; j < nshift; j += 2) {
+    /* B2: introduce bulge j */
+    const double sigma = sr[j] + sr[j + 1];
+    const double pi = sr[j] * sr[j + 1] - si[j] * si[j + 1];
+    const double h00 = IDX(H, ldh, 0, 0), h01 = IDX(H, ldh, 0, 1), h10 = IDX(H, ldh, 1, 0);
+    const double h11 = IDX(H, ldh, 1, 1), h21 = IDX(H, ldh, 2, 1);
+    double alpha = h00 * h00 + h01 * h10 - sigma * h00 + pi;
+    double x[2] = {h10 * (h00 + h11 - sigma), h10 * h21};
+    double tau;
+    or_larfg3(&alpha, x, &tau);
+    double v[3] = {1.0, x[0], x[1]};
+    refl_left_m(H, ldh, 3, 0, 0, n, v, tau);
+    refl_right_m(H, ldh, 3, 0, 0, n < 4 ? n : 4, v, tau);
+    if (Q) refl_right_m(Q, ldq, 3, 0, 0, nq, v, tau);
+    /* B3: chase it to the bottom */
+    for (int64_t p = 1; p <= n - 2; ++p) {
+      const int m = p <= n - 3 ? 3 : 2;
+      alpha = IDX(H, ldh, p, p - 1);
+      if (m == 3) {
+        x[0] = IDX(H, ldh, p + 1, p - 1);
+        x[1] = IDX(H, ldh, p + 2, p - 1);
+        or_larfg3(&alpha, x, &tau);
+        v[0] = 1.0; v[1] = x[0]; v[2] = x[1];
+      } else {
+        x[0] = IDX(H, ldh, p + 1, p - 1);
+        or_larfg2(&alpha, &x[0], &tau);
+        v[0] = 1.0; v[1] = x[0]; v[2] = 0.0;
+      }
+      IDX(H, ldh, p, p - 1) = alpha;
+      for (int i = 1; i < m; ++i) IDX(H, ldh, p + i, p - 1) = 0.0;
+      refl_left_m(H, ldh, m, p, p, n, v, tau);
+      const int64_t r1 = p + 4 < n ? p + 4 : n;
+      refl_right_m(H, ldh, m, p, 0, r1, v, tau);
+      if (Q) refl_right_m(Q, ldq, m, p, 0, nq, v, tau);
+    }
+  }
   return 0;
 }

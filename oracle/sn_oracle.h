@@ -176,6 +176,14 @@ int or_eig_count(int64_t n, const double* S, int64_t lds, const int32_t* select,
 int or_eigvec(int64_t n, const double* S, int64_t lds, const double* Q, int64_t ldq, const int32_t* select,
               double* X, int64_t ldx, int32_t* scale_exp);
 
+/* ---- bulge-chasing sweep of multishift QR (Table 1).
+ * Readings B1-B5 in sn_oracle.c and DESIGN.md §3.3.  One sweep with nshift (even) shifts
+ * sr + i si in pairs (two real shifts or a conjugate pair) on the upper Hessenberg H:
+ * H <- U^T H U (Hessenberg again), Q <- Q U (Q: nq <= n rows, may be NULL).  Bulges are
+ * introduced and chased to the bottom one after another (B4).  Returns 0 or -i. */
+int or_qr_sweep(int64_t n, double* H, int64_t ldh, double* Q, int64_t ldq, int64_t nq, int64_t nshift,
+                const double* sr, const double* si);
+
 #ifdef __cplusplus
 }
 #endif
