@@ -214,6 +214,85 @@ int sn_reorder_pencil_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS,
 /* Library version string. */
 const char* sn_version(void);
 
+/* ---- eigenvectors ----
+ * PAPER.md Eq. (5): for every selected eigenvalue lambda of the real Schur form S,
+ * a vector y with (S - lambda I) y = 0, computed by back substitution "protected against
+ * floating-point overflow"; Eq. (6): the back-transform x = Q y.
+ * Readings E1-E6: one column per selected 1x1 block, two (real part,
+ * imaginary part of the eigenvector of lambda = a + i w, w > 0) per selected 2x2 block, in
+ * block order; the block's own entries as LAPACK xTREVC; overflow protection by power-of-two
+ * scalings keeping every stored value <= 2^500; each column (pair) normalised so that
+ * max_i (|re_i| + |im_i|) = 1 (xTREVC).
+ *
+ * n: order; S: DEVICE pointer, n x n, ldS >= n, upper quasi-triangular in standard form (2x2
+ * blocks [a b; c a], bc < 0: the output of sn_reorder_schur); Q: DEVICE n x n (ldQ >= n) or
+ * NULL (X = Y, the Schur-basis vectors); select: HOST int32[n] (nonzero = selected; a 2x2
+ * block if either row is); X: DEVICE n x ncols (ldX >= n) output, or NULL to query *ncols
+ * only; ncols: out; scale_exp: HOST int32[ncols] or NULL: per column the e of the
+ * protective scaling 2^-e applied before the normalisation; stats: optional; stream: the
+ * CUDA stream (NULL: legacy default).  Synchronous with respect to the host.  Returns 0, -i
+ * for argument i (-2 also if S is not quasi-triangular or not a device pointer),
+ * SN_ERR_CUDA.  The library owns an n x ncols FP64 workspace when Q is given. */
+typedef struct sn_eig_stats {
+  int64_t columns;           /* columns of X */
+  int64_t vectors;           /* eigenvectors (a complex pair counts once) */
+  int64_t tiles;             /* row tiles of the blocked back substitution */
+  int64_t rescales;          /* protective power-of-two rescalings performed */
+  int64_t launches;          /* kernel launches */
+  double flops_solve;        /* diagonal-tile back substitution flops */
+  double flops_update;       /* off-diagonal update GEMM flops (2 i0 x tile x columns) */
+  double flops_backtransform;/* X = Q Y GEMM flops (2 n x K extent x columns) */
+  double ms_backsubstitution, ms_backtransform, ms_normalize, ms_device, ms_total;
+} sn_eig_stats;
+
+int sn_eigenvectors(int64_t n, const double* S, int64_t ldS, const double* Q, int64_t ldQ,
+                    const int32_t* select, double* X, int64_t ldX, int64_t* ncols,
+                    int32_t* scale_exp, sn_eig_stats* stats, void* stream);
+
+/* ---- one bulge-chasing sweep of the multishift QR algorithm ----
+ * bulges created at the top of the upper Hessenberg H and chased down the
+ * diagonal by overlapping 3 x 3 Householder reflectors to complete one pipelined QR iteration
+ * (Table 1).  Readings B1-B5: nshift (even) shifts sr[j] + i si[j] in
+ * pairs (two real shifts, or a complex conjugate pair with sr equal and si opposite); pair j
+ * makes bulge j, introduced by the reflector of (H^2 - sigma H + pi I) e1; the reflectors
+ * follow xLARFG; the entries they annihilate are set to exact zeros.  On return
+ * H <- U^T H U (upper Hessenberg) and Q <- Q U.
+ *
+ * Execution: chains of up to bulges_per_chain bulges spaced 4 rows apart, chased through
+ * overlapping diagonal windows of <= window rows; each window's reflectors are accumulated
+ * into a window-sized U and applied to the row panel right of the window, the column panel
+ * above it and the columns of Q by the reordering's DMMA panel kernels (Fig. 1b).
+ *
+ * n: order; H: DEVICE n x n, ldH >= n, upper Hessenberg (exact zeros below the subdiagonal,
+ * checked: -2 otherwise); Q: DEVICE n x n (ldQ >= n) or NULL; sr, si: HOST arrays of nshift
+ * doubles; opts: NULL for the defaults; stats: optional; stream: CUDA stream (NULL: legacy
+ * default).  Synchronous with respect to the host.  Returns 0, -i for argument i,
+ * SN_ERR_CUDA, SN_ERR_UNSUPPORTED (window < 16 or > 256, or a chain that does not fit:
+ * 4 (bulges_per_chain - 1) + 8 > window). */
+typedef struct sn_sweep_opts {
+  int64_t window;            /* rows of a window, 16..256 (default 256) */
+  int64_t bulges_per_chain;  /* bulges chased together, 1..60 (default 32) */
+  int32_t q_stream_overlap;  /* 1 (default): Q updates on a second stream */
+  int32_t reserved;
+} sn_sweep_opts;
+
+typedef struct sn_sweep_stats {
+  int64_t windows, levels, chains, bulges, launches;
+  double eq_flops;           /* equivalent update flops: per window 2k^2 ((n-j2) + j1 + n_Q) */
+  double flops_left, flops_right, flops_q;
+  double ms_device, ms_total;
+} sn_sweep_stats;
+
+void sn_sweep_default_opts(sn_sweep_opts* o);
+int sn_qr_sweep(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64_t nshift,
+                const double* sr, const double* si, const sn_sweep_opts* opts,
+                sn_sweep_stats* stats, void* stream);
+
+/* Host-only: the windows of one sweep (rows [w0, w0+k), DAG level), in sequential order.
+ * Pass NULL arrays to query the counts. */
+int sn_sweep_schedule(int64_t n, int64_t nshift, int64_t window, int64_t bulges_per_chain,
+                      int64_t* nwin, int64_t* nlevels, int64_t* w0, int64_t* k, int64_t* level);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,7 +75,34 @@ SN_OK, SN_ERR_REJECTED, SN_ERR_CUDA, SN_ERR_NCCL, SN_ERR_UNSUPPORTED = 0, 1, 2, 
 EXPORTS = ["sn_default_opts", "sn_strerror", "sn_reorder_schur", "sn_reorder_schur_ex",
            "sn_schedule_build", "sn_schedule_lookahead", "sn_schedule_window_swaps", "sn_version",
            "sn_dist_unique_id", "sn_dist_init", "sn_dist_finalize", "sn_dist_layout", "sn_reorder_schur_dist",
-           "sn_reorder_schur_dist_local", "sn_dist_program", "sn_release_workspace", "sn_reorder_pencil_ex"]
+           "sn_reorder_schur_dist_local", "sn_dist_program", "sn_release_workspace", "sn_reorder_pencil_ex",
+           "sn_eigenvectors", "sn_sweep_default_opts", "sn_qr_sweep", "sn_sweep_schedule"]
+
+
+class SweepOpts(C.Structure):
+    _fields_ = [("window", C.c_int64), ("bulges_per_chain", C.c_int64), ("q_stream_overlap", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class SweepStats(C.Structure):
+    _fields_ = [("windows", C.c_int64), ("levels", C.c_int64), ("chains", C.c_int64), ("bulges", C.c_int64),
+                ("launches", C.c_int64), ("eq_flops", C.c_double), ("flops_left", C.c_double),
+                ("flops_right", C.c_double), ("flops_q", C.c_double), ("ms_device", C.c_double),
+                ("ms_total", C.c_double)]
+
+    def to_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class EigStats(C.Structure):
+    _fields_ = [("columns", C.c_int64), ("vectors", C.c_int64), ("tiles", C.c_int64), ("rescales", C.c_int64),
+                ("launches", C.c_int64), ("flops_solve", C.c_double), ("flops_update", C.c_double),
+                ("flops_backtransform", C.c_double), ("ms_backsubstitution", C.c_double),
+                ("ms_backtransform", C.c_double), ("ms_normalize", C.c_double), ("ms_device", C.c_double),
+                ("ms_total", C.c_double)]
+
+    def to_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 _lib = None
 
@@ -123,6 +150,13 @@ def lib():
         L.sn_reorder_pencil_ex.argtypes = [C.POINTER(Opts), i64, p, i64, p, i64, p, i64, p, i64, p, C.POINTER(i64),
                                            p, C.POINTER(Stats), p]
         L.sn_reorder_pencil_ex.restype = C.c_int
+        L.sn_eigenvectors.argtypes = [i64, p, i64, p, i64, p, p, i64, C.POINTER(i64), p, C.POINTER(EigStats), p]
+        L.sn_eigenvectors.restype = C.c_int
+        L.sn_sweep_default_opts.argtypes = [C.POINTER(SweepOpts)]
+        L.sn_qr_sweep.argtypes = [i64, p, i64, p, i64, i64, p, p, C.POINTER(SweepOpts), C.POINTER(SweepStats), p]
+        L.sn_qr_sweep.restype = C.c_int
+        L.sn_sweep_schedule.argtypes = [i64, i64, i64, i64, C.POINTER(i64), C.POINTER(i64), p, p, p]
+        L.sn_sweep_schedule.restype = C.c_int
         _lib = L
     return _lib
 
@@ -182,6 +216,69 @@ def reorder(S, Q, select, window: int = 256, stream=None, **opts):
                                    bmap.ctypes.data_as(C.c_void_p), C.byref(st),
                                    None if stream is None else C.c_void_p(stream))
     return {"rc": rc, "m": m.value, "select": sel, "bmap": bmap, "stats": st.to_dict()}
+
+
+def eigenvectors(S, Q, select, stream=None, scale_exp=False):
+    """Right eigenvectors of the selected blocks of the real Schur form S (Eq. (5)),
+    back-transformed by Q (Eq. (6)) if given (sn_eigenvectors, row f4).  S, Q: CUDA fp64
+    tensors holding the transposed (column-major) matrices.  Returns dict(rc, X, ncols,
+    scale_exp, stats); X is a CUDA tensor of shape (ncols, n) holding X^T (column j of X is
+    row j of the tensor)."""
+    import torch
+    ps, n = _tensor_ptr(S)
+    pq, nq = _tensor_ptr(Q)
+    assert Q is None or nq == n
+    sel = np.ascontiguousarray(select, np.int32)
+    nc = C.c_int64()
+    L = lib()
+    if stream is None and S.is_cuda:
+        stream = torch.cuda.current_stream(S.device).cuda_stream
+    sv = None if stream is None else C.c_void_p(stream)
+    rc = L.sn_eigenvectors(n, ps, n, pq, n, sel.ctypes.data_as(C.c_void_p), None, n, C.byref(nc), None, None, sv)
+    if rc:
+        return {"rc": rc, "X": None, "ncols": 0, "scale_exp": None, "stats": None}
+    X = torch.empty((max(nc.value, 1), n), dtype=torch.float64, device=S.device)
+    e = np.zeros(max(nc.value, 1), np.int32)
+    st = EigStats()
+    rc = L.sn_eigenvectors(n, ps, n, pq, n, sel.ctypes.data_as(C.c_void_p), C.c_void_p(X.data_ptr()), n,
+                           C.byref(nc), e.ctypes.data_as(C.c_void_p) if scale_exp else None, C.byref(st), sv)
+    return {"rc": rc, "X": X[:nc.value], "ncols": nc.value, "scale_exp": e[:nc.value] if scale_exp else None,
+            "stats": st.to_dict()}
+
+
+def qr_sweep(H, Q, sr, si, stream=None, **opts):
+    """One multishift QR bulge-chasing sweep in place (sn_qr_sweep, row f3).  H, Q: CUDA fp64
+    tensors holding the transposed (column-major) matrices; Q may be None.  sr, si: the
+    shifts.  Returns dict(rc, stats)."""
+    import torch
+    ph, n = _tensor_ptr(H)
+    pq, nq = _tensor_ptr(Q)
+    assert Q is None or nq == n
+    o = SweepOpts()
+    lib().sn_sweep_default_opts(C.byref(o))
+    for k, v in opts.items():
+        setattr(o, k, v)
+    sr = np.ascontiguousarray(sr, np.float64)
+    si = np.ascontiguousarray(si, np.float64)
+    st = SweepStats()
+    if stream is None and H.is_cuda:
+        stream = torch.cuda.current_stream(H.device).cuda_stream
+    rc = lib().sn_qr_sweep(n, ph, n, pq, n, len(sr), sr.ctypes.data_as(C.c_void_p), si.ctypes.data_as(C.c_void_p),
+                           C.byref(o), C.byref(st), None if stream is None else C.c_void_p(stream))
+    return {"rc": rc, "stats": st.to_dict()}
+
+
+def sweep_schedule(n: int, nshift: int, window: int = 256, bulges_per_chain: int = 32):
+    """Host-only: the windows of one sweep (w0, k, level) in sequential order."""
+    nw, nl = C.c_int64(), C.c_int64()
+    L = lib()
+    rc = L.sn_sweep_schedule(n, nshift, window, bulges_per_chain, C.byref(nw), C.byref(nl), None, None, None)
+    if rc:
+        raise ValueError("sn_sweep_schedule rc=%d" % rc)
+    w0, k, lev = (np.zeros(nw.value, np.int64) for _ in range(3))
+    L.sn_sweep_schedule(n, nshift, window, bulges_per_chain, C.byref(nw), C.byref(nl), w0.ctypes.data_as(C.c_void_p),
+                        k.ctypes.data_as(C.c_void_p), lev.ctypes.data_as(C.c_void_p))
+    return {"w0": w0, "k": k, "level": lev, "nlevels": nl.value}
 
 
 def reorder_pencil(S, T, Q, Z, select, window: int = 256, stream=None, **opts):

@@ -297,3 +297,85 @@ def make_pencil(n: int, p2: float = 0.25, q: str = "householder", sel: str = "be
         Z = None
     meta = dict(base.meta, kind="pencil")
     return Pencil(n=n, S=base.S, T=Tt, Q=base.Q, Z=Z, select=base.select, w=w, bsizes=sizes, meta=meta)
+
+
+# ---- Hessenberg inputs for the bulge-chasing sweep --------------------
+_ST_HESS = 13
+
+
+@dataclasses.dataclass
+class Hessenberg:
+    n: int
+    H: torch.Tensor            # (n, n) row-major tensor holding H^T (= column-major H)
+    Q: torch.Tensor | None     # same layout, or None
+    sr: np.ndarray             # shifts, real parts (pairs: B1)
+    si: np.ndarray             # imaginary parts
+    meta: dict
+
+    def H_np(self) -> np.ndarray:
+        return self.H.cpu().numpy().T
+
+    def Q_np(self):
+        return None if self.Q is None else self.Q.cpu().numpy().T
+
+
+def shift_pairs(eigs) -> tuple[np.ndarray, np.ndarray]:
+    """Order eigenvalue estimates as shift pairs (reading B1): each complex conjugate pair
+    together (positive imaginary part first), the real ones paired in sorted order."""
+    eigs = np.asarray(eigs)
+    cplx = sorted([e for e in eigs if e.imag > 0], key=lambda e: (e.real, e.imag))
+    real = sorted([e.real for e in eigs if e.imag == 0])
+    sr, si = [], []
+    for e in cplx:
+        sr += [e.real, e.real]
+        si += [e.imag, -e.imag]
+    if len(real) % 2:
+        real = real[:-1]
+    sr += real
+    si += [0.0] * len(real)
+    return np.array(sr, np.float64), np.array(si, np.float64)
+
+
+def make_hessenberg(n: int, ns: int, q: str = "householder", seed: int = 1, device="cpu",
+                    shifts: str = "random") -> Hessenberg:
+    """A random upper Hessenberg matrix (entries on and above the subdiagonal iid N(0, 1),
+    exact zeros below: a stand-in for the Hessenberg form of the paper's random test matrices,
+    P:313), Q = I or the Householder product of make_problem, and ns shifts:
+      * "random": ns/2 complex conjugate pairs, real part U[-2, 2], imaginary part U[0.1, 2]
+        (seeded; the sweep's result is then a well-conditioned function of its input, so it
+        is compared elementwise);
+      * "trailing": the eigenvalues of the trailing ns x ns block (the xLAQR0 fall-back shift
+        strategy, computed with numpy -- input generation, not the method).  Good shifts make
+        subdiagonal entries nearly vanish, where the sweep's output is ill-conditioned (even
+        LAPACK's xLAQR5 and the oracle then differ at O(1)): checked by invariants only."""
+    device = torch.device(device)
+    Ht = torch.empty((n, n), dtype=torch.float64, device=device)   # Ht[j, i] = H[i, j]
+    rows = torch.arange(n, device=device, dtype=torch.int64)
+    for c0 in range(0, n, 1024):
+        c1 = min(n, c0 + 1024)
+        cols = torch.arange(c0, c1, device=device, dtype=torch.int64)
+        val = normal(seed, _ST_HESS, cols[:, None] * n + rows[None, :])
+        Ht[c0:c1] = torch.where(rows[None, :] <= cols[:, None] + 1, val, torch.zeros((), dtype=val.dtype, device=device))
+    if q == "identity":
+        Q = torch.eye(n, dtype=torch.float64, device=device)
+    elif q == "householder":
+        Q = _householder_product_T(n, seed, device)
+    elif q == "none":
+        Q = None
+    else:
+        raise ValueError(q)
+    if shifts == "random":
+        npair = ns // 2
+        re = -2.0 + 4.0 * _uni_np(seed, _ST_HESS + 1, np.arange(npair))
+        im = 0.1 + 1.9 * _uni_np(seed, _ST_HESS + 2, np.arange(npair))
+        sr = np.repeat(re, 2)
+        si = np.stack([im, -im], 1).reshape(-1)
+    elif shifts == "trailing":
+        m = min(ns, n)
+        tail = Ht[n - m:, n - m:].cpu().numpy().T
+        sr, si = shift_pairs(np.linalg.eigvals(tail))
+    else:
+        raise ValueError(shifts)
+    meta = dict(n=n, ns=len(sr), q=q, seed=seed, shifts=shifts)
+    return Hessenberg(n=n, H=Ht, Q=Q, sr=np.ascontiguousarray(sr, np.float64),
+                      si=np.ascontiguousarray(si, np.float64), meta=meta)
