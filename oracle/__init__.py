@@ -238,8 +238,8 @@ def gswap(S, T, j: int, n1: int, n2: int, Ql=None, Zr=None):
 
 
 def gswap_last_variant() -> int:
-    """Which branch the last gswap() took: 0 G1, 1 left / 2 right re-triangularisation
-    kept (G2), -1 rejected."""
+    """Which branch the last gswap() took: 0 G1, 1 the Sylvester pair (U0, V0), 2 the left /
+    3 the right re-triangularisation kept (G2/G3), -1 rejected."""
     return lib().or_gswap_last_variant()
 
 

@@ -811,19 +811,22 @@ int or_reorder_q(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t
  *         S11 R - L S22 = S12,  T11 R - L T22 = T12   (scale 1)
  *       by Gaussian elimination with complete pivoting on its Kronecker
  *       form (order 2 n1 n2); orthogonal bases V0 of span[-R; I] (right) and
- *       U0 of span[-L; I] (left) by Householder QR.  Then, as xTGEX2 does on
- *       every swap, T's block is re-triangularised both ways -- from the left
- *       (U from a QR of the first n2 columns of T V0, V = V0) and from the
- *       right (V completing the row space of the last n1 rows of U0^T T,
- *       U = U0) -- so that T's block below the new leading block is zero to
- *       working accuracy, and the variant whose S block there is smaller
- *       (Frobenius norm; ties to the left variant) is kept.
- *   G3  weak stability test: 1x1|1x1: |s21| and |t21| after the swap at most
- *       max(20 eps ||block||_F, smlnum) of their matrix's block; other cases:
- *       the kept variant's n1 x n2 S block below the new leading block at
- *       most max(20 eps ||S block||_F, smlnum) (xTGEX2's test; T's is zero by
- *       construction).  Otherwise the swap is rejected (nothing is changed);
- *       passed blocks are set to exact zeros.
+ *       U0 of span[-L; I] (left) by Householder QR.  Three candidate factor
+ *       pairs: (U0, V0) itself, and the two re-triangularisations of T's
+ *       block that xTGEX2 uses -- from the left (U from a QR of the first n2
+ *       columns of T V0, V = V0) and from the right (V completing the row
+ *       space of the last n1 rows of U0^T T, U = U0) -- which make T's block
+ *       below the new leading block zero to working accuracy.
+ *   G3  weak stability test: a candidate's residual is max(||S21||_F /
+ *       threshA, ||T21||_F / threshB) over the blocks below the new leading
+ *       block, thresh = max(20 eps ||block||_F, smlnum); the candidate with
+ *       the smallest residual is kept (ties: the earlier one) and the swap is
+ *       rejected (nothing changed) if that residual exceeds 1.  (1x1|1x1:
+ *       the G1 pair, both blocks tested.)  Passed blocks become exact zeros.
+ *       (The Sylvester pair's own residual governs (U0, V0): it passes where
+ *       the re-triangularised variants lose accuracy to a large R, L, and
+ *       vice versa; keeping the best of the three rejects fewer well-
+ *       conditioned swaps than either rule alone -- DESIGN.md §3.1.)
  *   G4  standard form: every 2x2 diagonal block of T is diagonal with
  *       t11 >= t22 > 0 (a 2x2 SVD applied to both matrices); the paired
  *       2x2 block of S is left general; a moved 1x1 block has t >= 0.  A moved 2x2 block whose pencil has
@@ -1042,7 +1045,7 @@ static int std_t22(const double* Tb, double* P, double* W) {
   return 0;
 }
 
-static int g_gswap_variant = 0;   /* diagnostics: 0 G1, 1 left variant kept, 2 right, -1 rejected */
+static int g_gswap_variant = 0;   /* diagnostics: 0 G1, 1 (U0, V0), 2 left, 3 right variant kept, -1 rejected */
 int or_gswap_last_variant(void) { return g_gswap_variant; }
 
 int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t j, int n1, int n2,
@@ -1126,22 +1129,34 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
       for (int r = 0; r < m; ++r) Vr[r + 4 * c] = H[r + 4 * (n1 + c)];
     for (int c = 0; c < n1; ++c)
       for (int r = 0; r < m; ++r) Vr[r + 4 * (n2 + c)] = H[r + 4 * c];
-    double Aq[16], Ar[16];
-    sm_congruence(Uq, A, V0, Aq, m);
-    sm_congruence(U0, A, Vr, Ar, m);
-    const double rq = lowblock_fro(Aq, n1, n2), rr = lowblock_fro(Ar, n1, n2);
-    if (rq <= rr) { memcpy(U, Uq, sizeof(Uq)); memcpy(V, V0, sizeof(V0)); }
-    else { memcpy(U, U0, sizeof(U0)); memcpy(V, Vr, sizeof(Vr)); }
-    g_gswap_variant = rq <= rr ? 1 : 2;
+    /* G3: each candidate's residual, max(||S21|| / threshA, ||T21|| / threshB); keep the
+     * smallest (ties: the earlier candidate) */
+    const double* cu[3] = {U0, Uq, U0};
+    const double* cv[3] = {V0, V0, Vr};
+    double best = 0.0;
+    int bi = -1;
+    for (int q = 0; q < 3; ++q) {
+      double Aq[16], Bq[16];
+      sm_congruence(cu[q], A, cv[q], Aq, m);
+      sm_congruence(cu[q], B, cv[q], Bq, m);
+      const double r = dmax(lowblock_fro(Aq, n1, n2) / threshA, lowblock_fro(Bq, n1, n2) / threshB);
+      if (bi < 0 || r < best) { best = r; bi = q; }
+    }
+    memcpy(U, cu[bi], sizeof(U0));
+    memcpy(V, cv[bi], sizeof(V0));
+    g_gswap_variant = bi + 1;
+    if (!(best <= 1.0)) { g_gswap_variant = -1; return 1; }
   }
   double An[16], Bn[16];
   sm_congruence(U, A, V, An, m);
   sm_congruence(U, B, V, Bn, m);
-  /* G3 */
-  const double resA = lowblock_fro(An, n1, n2), resB = lowblock_fro(Bn, n1, n2);
-  if (n1 == 1 && n2 == 1 ? !(resA <= threshA && resB <= threshB) : !(resA <= threshA)) {
-    g_gswap_variant = -1;
-    return 1;
+  if (n1 == 1 && n2 == 1) {
+    /* G3 (1x1|1x1): both blocks below the new leading block */
+    const double resA = lowblock_fro(An, n1, n2), resB = lowblock_fro(Bn, n1, n2);
+    if (!(resA <= threshA && resB <= threshB)) {
+      g_gswap_variant = -1;
+      return 1;
+    }
   }
   for (int c = 0; c < n2; ++c)
     for (int r = n2; r < m; ++r) { An[r + 4 * c] = 0.0; Bn[r + 4 * c] = 0.0; }

@@ -147,7 +147,8 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
              double* Ql, int64_t ldq, int64_t nq, double* Zr, int64_t ldz, int64_t nz);
 
 /* Diagnostics of the last or_gswap call (not thread-safe): 0 a 1x1|1x1 swap (G1), 1 the
- * left re-triangularisation kept (G2), 2 the right one kept, -1 rejected (G3/G4). */
+ * Sylvester pair (U0, V0) kept, 2 the left re-triangularisation, 3 the right one (G2/G3),
+ * -1 rejected (G3/G4). */
 int or_gswap_last_variant(void);
 
 /* Generalized reordering (S, T) = Q3 (Ŝ, T̂) Z3^T, Q <- Q Q3, Z <- Z Z3 (Q, Z may be

@@ -304,10 +304,9 @@ __host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double
     else pl_lartg(bx0, bx1, c2, s2, r2);
     U[0] = c2; U[1] = s2; U[4] = -s2; U[5] = c2;
   } else {
-    // G2: Sylvester bases V0, U0, then both re-triangularisations of T's block (xTGEX2): from
+    // G2: Sylvester bases V0, U0, and the two re-triangularisations of T's block (xTGEX2): from
     // the left (U from the QR of (T V0)(:, 1:n2), V = V0) and from the right (V completing the
-    // row space of (U0^T T)(n2+1:m, :), U = U0); keep the one whose S block below the new
-    // leading block is smaller (ties: the left one)
+    // row space of (U0^T T)(n2+1:m, :), U = U0)
     double R[4] = {0.0, 0.0, 0.0, 0.0}, L[4] = {0.0, 0.0, 0.0, 0.0};
     pl_gsylv<N1, N2>(A, B, R, L);
     double Mr[16], Ml[16], U0[16], V0[16];
@@ -348,22 +347,36 @@ __host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double
     for (int c = 0; c < n1; ++c)
 #pragma unroll
       for (int r = 0; r < m; ++r) Vr[r + 4 * (n2 + c)] = H[r + 4 * c];
-    pl_congr(Uq, A, V0, Aq, m);
-    pl_congr(U0, A, Vr, Ar, m);
-    const double rq = pl_lowfro(Aq, n1, n2), rr = pl_lowfro(Ar, n1, n2);
-    const bool left = rq <= rr;
+    // G3: each candidate's residual max(||S21|| / thA, ||T21|| / thB); keep the smallest (ties:
+    // the earlier) -- the Sylvester pair (U0, V0), the left and the right re-triangularisation
+    double best = 0.0;
+    int bi = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) { U[i] = left ? Uq[i] : U0[i]; V[i] = left ? V0[i] : Vr[i]; }
+    for (int q = 0; q < 3; ++q) {
+      const double* cu = q == 1 ? Uq : U0;
+      const double* cv = q == 2 ? Vr : V0;
+      pl_congr(cu, A, cv, Aq, m);
+      pl_congr(cu, B, cv, Ar, m);
+      const double r = fmax(pl_lowfro(Aq, n1, n2) / thA, pl_lowfro(Ar, n1, n2) / thB);
+      if (q == 0 || r < best) { best = r; bi = q; }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      U[i] = bi == 1 ? Uq[i] : U0[i];
+      V[i] = bi == 2 ? Vr[i] : V0[i];
+    }
+    if (!(best <= 1.0)) {
+      if (why) { why[0] = 1.0; why[1] = best; }
+      return false;
+    }
   }
   pl_congr(U, A, V, An, m);
   pl_congr(U, B, V, Bn, m);
-  // G3 (xTGEX2's weak test): 1x1|1x1 both blocks below the new leading block; otherwise S's
-  // (T's is zero by the re-triangularisation)
-  {
+  if (n1 == 1 && n2 == 1) {
+    // G3 (1x1|1x1): both blocks below the new leading block
     const double resA = pl_lowfro(An, n1, n2), resB = pl_lowfro(Bn, n1, n2);
-    const bool pass = (n1 == 1 && n2 == 1) ? (resA <= thA && resB <= thB) : (resA <= thA);
-    if (!pass) {
-      if (why) { why[0] = 1.0; why[1] = (n1 == 1 && n2 == 1) ? fmax(resA / thA, resB / thB) : resA / thA; }
+    if (!(resA <= thA && resB <= thB)) {
+      if (why) { why[0] = 1.0; why[1] = fmax(resA / thA, resB / thB); }
       return false;
     }
   }

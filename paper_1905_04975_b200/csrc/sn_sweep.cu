@@ -63,7 +63,15 @@ __device__ __forceinline__ void larfg(int m, double& alpha, double& x0, double& 
   alpha = beta;
 }
 
+// STAGED: the window (k <= kStageMax) is copied to shared memory, worked on there and written
+// back (the per-step left/right updates then cost shared-memory latency, not L2 round trips);
+// otherwise it is updated in place in global memory (L2 resident).
+constexpr int kStageMax = 160;
+constexpr int kStageLd = kStageMax + 1;   // odd stride: conflict-free row walks
+
+template <bool STAGED>
 __global__ void __launch_bounds__(kSweepThreads, 1) bulge_window_kernel(SweepArgs a) {
+  extern __shared__ __align__(16) double hs[];
   __shared__ double rv[kMaxChainBulges][3];
   __shared__ double rt[kMaxChainBulges];
   __shared__ int rp[kMaxChainBulges];    // local first row of the reflector, -1 inactive
@@ -73,8 +81,16 @@ __global__ void __launch_bounds__(kSweepThreads, 1) bulge_window_kernel(SweepArg
   const WinDev wd = a.wins[blockIdx.x];
   const BulgeDev bd = a.bw[blockIdx.x];
   const int k = wd.k;
-  const int64_t w0 = wd.j1, ld = a.ldH, n = a.n;
-  double* Hw = a.H + w0 + w0 * ld;                   // local (r, c) at Hw[r + c * ld]
+  const int64_t w0 = wd.j1, n = a.n;
+  double* Hg = a.H + w0 + w0 * a.ldH;                 // the window in global memory
+  double* Hw = STAGED ? hs : Hg;                      // local (r, c) at Hw[r + c * ld]
+  const int64_t ld = STAGED ? kStageLd : a.ldH;
+  if (STAGED) {
+    for (int idx = tid; idx < k * k; idx += kSweepThreads) {
+      const int r = idx % k, c = idx / k;
+      hs[r + c * kStageLd] = Hg[r + (int64_t)c * a.ldH];
+    }
+  }
   double* Z = a.Z + (int64_t)wd.slot * kZslot;
   for (int idx = tid; idx < kZld * kZld; idx += kSweepThreads) {
     const int r = idx & (kZld - 1), c = idx >> 8;
@@ -169,6 +185,12 @@ __global__ void __launch_bounds__(kSweepThreads, 1) bulge_window_kernel(SweepArg
       }
     }
     __syncthreads();
+  }
+  if (STAGED) {
+    for (int idx = tid; idx < k * k; idx += kSweepThreads) {
+      const int r = idx % k, c = idx / k;
+      Hg[r + (int64_t)c * a.ldH] = hs[r + c * kStageLd];
+    }
   }
   int16_t* zr = a.zrange + (int64_t)wd.slot * kZrange;
   for (int c = tid; c < kZld; c += kSweepThreads) { zr[c] = zlo[c]; zr[kZld + c] = zhi[c]; }
@@ -392,7 +414,18 @@ int sweep_run(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64_t
     sa.wins = (const WinDev*)ws.wins.p + a; sa.bw = (const BulgeDev*)ws.bw.p + a; sa.nwin = (int32_t)cnt;
     sa.H = H; sa.ldH = ldH; sa.n = n; sa.Z = dZ; sa.zrange = (int16_t*)ws.zr.p; sa.status = (int32_t*)ws.status.p;
     sa.sr = dsr; sa.si = dsi;
-    bulge_window_kernel<<<(unsigned)cnt, kSweepThreads, 0, sA>>>(sa);
+    if (W <= kStageMax) {
+      static bool attr[kMaxDevices] = {};
+      const int d = device_slot();
+      const size_t smem = sizeof(double) * (size_t)kStageLd * kStageMax;
+      if (!attr[d]) {
+        SK(cudaFuncSetAttribute(bulge_window_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr[d] = true;
+      }
+      bulge_window_kernel<true><<<(unsigned)cnt, kSweepThreads, smem, sA>>>(sa);
+    } else {
+      bulge_window_kernel<false><<<(unsigned)cnt, kSweepThreads, 0, sA>>>(sa);
+    }
     ++launches;
     SK(cudaGetLastError());
     if (overlapQ) SK(cudaEventRecord(ws.evW[gen], sA));

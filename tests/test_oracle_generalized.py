@@ -174,9 +174,10 @@ def test_gswap_matches_dtgexc(n1, n2):
     assert worst_proj <= 1e-12, worst_proj
     print((n1, n2), "variants kept:", variants)
     if (n1, n2) != (1, 1):
-        # both re-triangularisations of G2 (xTGEX2's QR and RQ variants) are exercised and
-        # each matches dtgexc (the former G2b branch had no pin)
-        assert variants.get(1, 0) >= 20 and variants.get(2, 0) >= 20, variants
+        # every G2 candidate -- the Sylvester pair and both re-triangularisations of xTGEX2 --
+        # is kept in some of these swaps, and each matches dtgexc (the former G2b
+        # branch had no pin)
+        assert min(variants.get(q, 0) for q in (1, 2, 3)) >= 5, variants
 
 
 def test_gswap_identity_T_is_the_standard_swap():
