@@ -94,6 +94,9 @@ typedef struct sn_stats {
   double flops_exec_kernel[5]; /* flops the panel kernels execute: Z^T row groups skip the K
                                   steps where Z is structurally zero; one-GPU
                                   executor only, else 0 */
+  double g3_max_ratio;       /* generalized path: the largest stability-test residual ratio
+                                (residual / threshold, G3) among the accepted swaps -- the
+                                decision margin; 0 elsewhere */
 } sn_stats;
 
 void sn_default_opts(sn_opts* o);
@@ -270,8 +273,9 @@ int sn_eigenvectors(int64_t n, const double* S, int64_t ldS, const double* Q, in
  * SN_ERR_CUDA, SN_ERR_UNSUPPORTED (window < 16 or > 256, or a chain that does not fit:
  * 4 (bulges_per_chain - 1) + 8 > window). */
 typedef struct sn_sweep_opts {
-  int64_t window;            /* rows of a window, 16..256 (default 256) */
-  int64_t bulges_per_chain;  /* bulges chased together, 1..60 (default 32) */
+  int64_t window;            /* rows of a window, 16..256 (default 160: <= 160 rows are staged
+                                in shared memory) */
+  int64_t bulges_per_chain;  /* bulges chased together, 1..60 (default 16) */
   int32_t q_stream_overlap;  /* 1 (default): Q updates on a second stream */
   int32_t reserved;
 } sn_sweep_opts;

@@ -819,7 +819,7 @@ int or_reorder_q(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t
  *       below the new leading block zero to working accuracy.
  *   G3  weak stability test: a candidate's residual is max(||S21||_F /
  *       threshA, ||T21||_F / threshB) over the blocks below the new leading
- *       block, thresh = max(20 eps ||block||_F, smlnum); the candidate with
+ *       block, thresh = max(100 eps ||block||_F, smlnum); the candidate with
  *       the smallest residual is kept (ties: the earlier one) and the swap is
  *       rejected (nothing changed) if that residual exceeds 1.  (1x1|1x1:
  *       the G1 pair, both blocks tested.)  Passed blocks become exact zeros.
@@ -1045,6 +1045,9 @@ static int std_t22(const double* Tb, double* P, double* W) {
   return 0;
 }
 
+/* G3's constant: SPEC's 10^2 eps acceptance constant for a direct swap
+ * (S:437); LAPACK xTGEX2 uses 20 */
+#define OR_G3_C 100.0
 static int g_gswap_variant = 0;   /* diagnostics: 0 G1, 1 (U0, V0), 2 left, 3 right variant kept, -1 rejected */
 int or_gswap_last_variant(void) { return g_gswap_variant; }
 
@@ -1066,8 +1069,8 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
   anorm = sqrt(anorm);
   bnorm = sqrt(bnorm);
   const double smlnum = DBL_MIN / DBL_EPSILON;
-  const double threshA = dmax(20.0 * DBL_EPSILON * anorm, smlnum);
-  const double threshB = dmax(20.0 * DBL_EPSILON * bnorm, smlnum);
+  const double threshA = dmax(OR_G3_C * DBL_EPSILON * anorm, smlnum);
+  const double threshB = dmax(OR_G3_C * DBL_EPSILON * bnorm, smlnum);
   double U[16], V[16];
   sm_eye(U, m);
   sm_eye(V, m);

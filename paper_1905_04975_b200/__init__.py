@@ -61,7 +61,8 @@ class Stats(C.Structure):
                 ("eq_flops", C.c_double), ("ms_schedule", C.c_double), ("ms_device", C.c_double),
                 ("ms_total", C.c_double), ("ms_h2d", C.c_double), ("ms_d2h", C.c_double),
                 ("launches", C.c_int64 * 5), ("ms_kernel", C.c_double * 5), ("flops_kernel", C.c_double * 5),
-                ("bytes_kernel", C.c_double * 5), ("flops_exec_kernel", C.c_double * 5)]
+                ("bytes_kernel", C.c_double * 5), ("flops_exec_kernel", C.c_double * 5),
+                ("g3_max_ratio", C.c_double)]
 
     def to_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing without a tool attached
 
 #include "sn_device.cuh"
 #include "sn_exec.h"
@@ -289,6 +290,8 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
   const double t_start = now_ms();
   int64_t launches[5] = {0, 0, 0, 0, 0};
   std::vector<std::pair<int, int>> prof_marks;   // (kind, first event index)
+  std::vector<std::pair<int64_t, int>> prof_lev;   // per mark: (level, stream: 0 critical, 1 rest, 2 Q)
+  int64_t cur_level = -1;
   size_t prof_used = 0;
   auto prof_begin = [&](int kind, cudaStream_t s) -> int {
     if (!o.profile) return -1;
@@ -301,6 +304,7 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
     prof_used += 2;
     cudaEventRecord(ws.prof[idx], s);
     prof_marks.push_back({kind, idx});
+    prof_lev.push_back({cur_level, s == ws.sC ? 1 : (s == ws.sB ? 2 : 0)});
     return idx;
   };
   auto prof_end = [&](int idx, cudaStream_t s) {
@@ -463,6 +467,8 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
   for (int64_t l = 0; l < P.nlevels; ++l) {
     const int64_t a = lstart[l], cnt = lstart[l + 1] - a;
     const int gen = (int)(l % kZgen);
+    cur_level = l;
+    nvtxRangePushA("sn level");
     if (overlapQ && l >= kZgen) CK(cudaStreamWaitEvent(sA, ws.evQ[gen], 0));
     WindowArgs wa{};
     wa.wins = dw + a; wa.nwin = (int32_t)cnt; wa.base = (int32_t)a;
@@ -541,6 +547,7 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
                              cudaMemcpyDeviceToHost, ws.sD));
       ho->copied = frontier[l];
     }
+    nvtxRangePop();
   }
   if (overlapQ) {
     CK(cudaEventRecord(ws.evJoin, sQ));
@@ -604,6 +611,21 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
   for (auto& pm : prof_marks) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ws.prof[pm.second], ws.prof[pm.second + 1]) == cudaSuccess) mk[pm.first] += ms;
+  }
+  // SN_TIMELINE=path (with opts.profile): every launch's start and end on its stream, from the
+  // CUDA events around it, relative to the start of the run -- the overlap evidence of the
+  // level executor (no nsys in this image)
+  if (const char* tl = std::getenv("SN_TIMELINE")) {
+    if (FILE* f = std::fopen(tl, "w")) {
+      std::fprintf(f, "kind,level,stream,start_ms,end_ms\n");
+      for (size_t q = 0; q < prof_marks.size(); ++q) {
+        float a0 = 0.f, a1 = 0.f;
+        cudaEventElapsedTime(&a0, ws.ev0, ws.prof[prof_marks[q].second]);
+        cudaEventElapsedTime(&a1, ws.ev0, ws.prof[prof_marks[q].second + 1]);
+        std::fprintf(f, "%d,%lld,%d,%.4f,%.4f\n", prof_marks[q].first, (long long)prof_lev[q].first, prof_lev[q].second, a0, a1);
+      }
+      std::fclose(f);
+    }
   }
   write_blocks(fsz, fsel, select, bmap_out);
   if (st) {

@@ -53,6 +53,8 @@ struct Control {
   int32_t rej_row;          // global first row of the rejected swap (pencil path)
   int32_t rej_n1, rej_n2;
   int32_t pad[2];
+  unsigned long long ratio_bits;  // pencil path: largest G3 residual ratio of an accepted swap
+                                  // (the bits of a non-negative double: ordered as integers)
 };
 
 // Per-window rejection record (standard path): a window that rejects a swap stores the number

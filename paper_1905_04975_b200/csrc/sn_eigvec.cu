@@ -35,15 +35,17 @@ namespace sn {
 namespace {
 
 constexpr double kOmega = 3.273390607896142e+150;   // 2^500 (E4)
-// a protective rescale brings the eigenvector down to 2^-256 of the bound (not just below it),
-// so that an exponentially growing vector rescales once per 2^256 of growth; the normalised
-// result is the same (power-of-two scalings), only the rescale count changes
-constexpr double kHeadroom = 8.636168555094445e-78;   // 2^-256
+// a protective rescale brings the eigenvector down to 2^-900 of the bound (not just below it),
+// so that an exponentially growing vector rescales once per 2^900 of growth; the normalised
+// result is the same (power-of-two scalings) up to entries below 2^-674 of the vector's
+// largest one, which may underflow to zero -- far below any comparison bar
+constexpr double kHeadroom = 1.18575755001e-271;   // 2^-900
 constexpr int kTileRows = 128;                        // nominal row tile (<= 129 with a 2x2 shift)
 constexpr int kTileMax = 130;
 constexpr int kLdT = kTileMax + 1;                    // odd stride of the staged diagonal tile
 constexpr int kRegs = 5;                              // rows per lane: 5 x 32 >= kTileMax
 constexpr int kSolveWarps = 16;
+constexpr int kSuper = 4;                             // row tiles per update super-tile
 
 struct EigUnit {
   int64_t k;      // first row of the eigenvalue's block
@@ -143,6 +145,17 @@ __device__ __forceinline__ int pow2_steps(double v, double lim) {
   return s;
 }
 
+// steps of a protective rescale for a growth bound g (in units of Omega, > 1): at least enough
+// to bring it to 1, as many as the headroom asks, but never below 2^-400 for the vector's
+// current magnitude ymag (a bound scaled by a huge matrix entry must not push the vector
+// itself into underflow)
+__device__ __forceinline__ int rescale_steps(double g, double ymag) {
+  const int smin = pow2_steps(g, 1.0);
+  int s = pow2_steps(g, kHeadroom);
+  if (ymag > 0.0) s = min(s, ilogb(ymag) + 400);
+  return max(s, smin);
+}
+
 // register j of the lane owning local row r: select without dynamic indexing
 __device__ __forceinline__ double reg_get(const double (&v)[kRegs], int j) {
   double x = v[0];
@@ -222,7 +235,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32, 1) eig_solve_kernel(SolveArg
       const double ym = fmax(cabs1(y0r, y0i), cabs1(y1r, y1i));
       const double g = fmax(((double)U.bs * (ym / kOmega)) * cm, (ym / kOmega) * a.snorm);
       if (g > 1.0) {
-        const int s = pow2_steps(g, kHeadroom);
+        const int s = rescale_steps(g, ym);
         const double f = ldexp(1.0, -s);
         y0r *= f; y0i *= f; y1r *= f; y1i *= f;
         e += s;
@@ -317,7 +330,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32, 1) eig_solve_kernel(SolveArg
     if (nb == 2) cm = fmax(cm, cmx[i + 1]);
     const double g = B / kOmega + ((double)nb * (ym / kOmega)) * cm;
     if (g > 1.0) {
-      const int s = pow2_steps(g, kHeadroom);
+      const int s = rescale_steps(g, fmax(fmax(B, ym), ynorm));
       const double f = ldexp(1.0, -s);
 #pragma unroll
       for (int j = 0; j < kRegs; ++j) { vr[j] *= f; vi[j] *= f; }
@@ -360,7 +373,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32, 1) eig_solve_kernel(SolveArg
   if (a.i0 > 0) {
     const double g = stt.bound / kOmega + (ynorm / kOmega) * a.snorm;
     if (g > 1.0) {
-      const int s = pow2_steps(g, kHeadroom);
+      const int s = rescale_steps(g, ynorm);
       const double f = ldexp(1.0, -s);
       __syncwarp();
       scale_rows(a.Y, a.ldY, U.col, ncol, 0, below1, f, lane);
@@ -543,6 +556,17 @@ __global__ void eig_normalize_kernel(double* X, int64_t ldX, int64_t rows, const
   }
 }
 
+// lambda of every unit: S[k, k] and, for a pair, S[k, k+1] and S[k+1, k]
+__global__ void eig_gather_kernel(const double* S, int64_t ldS, const int64_t* ks, const int8_t* bs, int nk,
+                                  double* out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nk) return;
+  const int64_t k = ks[q];
+  out[3 * q] = S[k + k * ldS];
+  out[3 * q + 1] = bs[q] == 2 ? S[k + (k + 1) * ldS] : 0.0;
+  out[3 * q + 2] = bs[q] == 2 ? S[(k + 1) + k * ldS] : 0.0;
+}
+
 __global__ void eig_exp_kernel(const EigUnit* units, const EigState* st, int nunits, int32_t* out) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= nunits) return;
@@ -641,15 +665,20 @@ int eigvec_run(int64_t n, const double* S, int64_t ldS, const double* Q, int64_t
       if (selrow[i]) ks.push_back(i);
       i += bs;
     }
-    // the block entries (diagonal and, for pairs, b and c) from the device
-    std::vector<double> blk(ks.size() * 3);
-    for (size_t q = 0; q < ks.size(); ++q) {
-      const int64_t k = ks[q];
-      EK(cudaMemcpyAsync(&blk[3 * q], S + k + k * ldS, 8, cudaMemcpyDeviceToHost, sA));
-      if (bmap[k] == 1) {
-        EK(cudaMemcpyAsync(&blk[3 * q + 1], S + k + (k + 1) * ldS, 8, cudaMemcpyDeviceToHost, sA));
-        EK(cudaMemcpyAsync(&blk[3 * q + 2], S + (k + 1) + k * ldS, 8, cudaMemcpyDeviceToHost, sA));
-      }
+    // the block entries (diagonal and, for pairs, b and c), gathered on the device
+    std::vector<double> blk(ks.size() * 3 + 3);
+    std::vector<int8_t> kb(ks.size() + 1);
+    for (size_t q = 0; q < ks.size(); ++q) kb[q] = bmap[ks[q]] == 1 ? 2 : 1;
+    if (!ks.empty()) {
+      EK(ws.units.ensure(ks.size() * (sizeof(int64_t) + 1 + 3 * sizeof(double)) + 64));
+      int64_t* dks = (int64_t*)ws.units.p;
+      double* dout = (double*)(dks + ks.size());
+      int8_t* dbs = (int8_t*)(dout + 3 * ks.size());
+      EK(cudaMemcpyAsync(dks, ks.data(), sizeof(int64_t) * ks.size(), cudaMemcpyHostToDevice, sA));
+      EK(cudaMemcpyAsync(dbs, kb.data(), ks.size(), cudaMemcpyHostToDevice, sA));
+      eig_gather_kernel<<<(unsigned)((ks.size() + 255) / 256), 256, 0, sA>>>(S, ldS, dks, dbs, (int)ks.size(), dout);
+      EK(cudaGetLastError());
+      EK(cudaMemcpyAsync(blk.data(), dout, sizeof(double) * 3 * ks.size(), cudaMemcpyDeviceToHost, sA));
     }
     EK(cudaStreamSynchronize(sA));
     int32_t col = 0;
@@ -719,6 +748,18 @@ int eigvec_run(int64_t n, const double* S, int64_t ldS, const double* Q, int64_t
   }
   // back substitution, bottom tile first
   double fl_solve = 0.0, fl_update = 0.0, fl_bt = 0.0;
+  // SN_EIG_PROFILE: events around every solve / GEMM launch (split of ms_backsubstitution)
+  const bool prof = std::getenv("SN_EIG_PROFILE") != nullptr;
+  std::vector<cudaEvent_t> pev;
+  std::vector<int> pkind;
+  auto mark = [&](int kind) {
+    if (!prof) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, sA);
+    pev.push_back(e);
+    pkind.push_back(kind);
+  };
   const int64_t kmax = units.back().k;
   int uA = nu;   // active units: k >= i0 (a suffix: units are sorted by k)
   for (int t = ntiles - 1; t >= 0; --t) {
@@ -732,7 +773,9 @@ int eigvec_run(int64_t n, const double* S, int64_t ldS, const double* Q, int64_t
     sa.units = (const EigUnit*)ws.units.p; sa.state = (EigState*)ws.state.p;
     sa.u0 = uA; sa.nu = na; sa.i0 = i0; sa.i1 = i1; sa.snorm = snorm[t];
     sa.rescales = (int32_t*)ws.cnt.p;
+    mark(0);
     eig_solve_kernel<<<(na + kSolveWarps - 1) / kSolveWarps, kSolveWarps * 32, smem_solve, sA>>>(sa);
+    mark(-1);
     ++launches;
     EK(cudaGetLastError());
     const int64_t colA = units[uA].col;
@@ -740,17 +783,31 @@ int eigvec_run(int64_t n, const double* S, int64_t ldS, const double* Q, int64_t
       const double rows = (double)(std::min(i1, units[q].k) - i0);
       fl_solve += 4.0 * units[q].bs * rows * rows;     // 2 flops per entry, complex = 2 real columns
     }
-    if (i0 > 0) {
+    // updates: within the super-tile (kSuper row tiles) the rows above this tile at once; the
+    // rows above the super-tile once its top tile is solved, with K = the super-tile's rows
+    // (a 4x longer K loop and a quarter of the passes over Y)
+    const int t0 = (t / kSuper) * kSuper;
+    const int64_t r0 = tb[t0];
+    auto gemm = [&](int64_t rlo, int64_t rhi, int64_t klo, int64_t khi) -> int {
+      if (rhi <= rlo) return 0;
       GemmArgs g{};
-      // A = S[0:i0, i0:i1] (columns from k0 = i0), B = Y[i0:i1, colA:], C = Y[0:i0, colA:]
-      g.A = S; g.lda = ldS;
+      // A = S[rlo:rhi, klo:khi] (columns from k0), B = Y[klo:khi, colA:], C = Y[rlo:rhi, colA:]
+      g.A = S + rlo; g.lda = ldS;
       g.B = Y + colA * ldY; g.ldb = ldY;
-      g.C = Y + colA * ldY; g.ldc = ldY;
-      g.M = i0; g.N = (int32_t)(nc - colA); g.k0 = i0; g.K = i1 - i0; g.kend = nullptr; g.minus = 1;
+      g.C = Y + colA * ldY + rlo; g.ldc = ldY;
+      g.M = rhi - rlo; g.N = (int32_t)(nc - colA); g.k0 = klo; g.K = khi - klo; g.kend = nullptr; g.minus = 1;
+      mark(1);
       launch_gemm(g, (g.N + GBN - 1) / GBN, sA);
+      mark(-1);
       ++launches;
       EK(cudaGetLastError());
-      fl_update += 2.0 * (double)i0 * (double)(i1 - i0) * (double)g.N;
+      fl_update += 2.0 * (double)(rhi - rlo) * (double)(khi - klo) * (double)g.N;
+      return 0;
+    };
+    if (int rc = gemm(r0, i0, i0, i1)) return rc;
+    if (t == t0) {
+      const int64_t s1 = tb[std::min(t0 + kSuper, ntiles)];
+      if (int rc = gemm(0, r0, r0, s1)) return rc;
     }
   }
   EK(cudaEventRecord(ws.ev[1], sA));
@@ -788,6 +845,17 @@ int eigvec_run(int64_t n, const double* S, int64_t ldS, const double* Q, int64_t
   int32_t cnt[4] = {0, 0, 0, 0};
   EK(cudaMemcpyAsync(cnt, ws.cnt.p, sizeof(cnt), cudaMemcpyDeviceToHost, sA));
   EK(cudaStreamSynchronize(sA));
+  if (prof) {
+    double acc[2] = {0.0, 0.0};
+    for (size_t q = 0; q + 1 < pev.size(); q += 2) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, pev[q], pev[q + 1]);
+      acc[pkind[q]] += ms;
+    }
+    for (auto e : pev) cudaEventDestroy(e);
+    std::fprintf(stderr, "{\"probe\":\"eigvec_phases\",\"ms_solve\":%.2f,\"ms_update_gemm\":%.2f,\"flops_update\":%.4g}\n",
+                 acc[0], acc[1], fl_update);
+  }
   if (st) {
     float a = 0.f, b = 0.f, c = 0.f;
     cudaEventElapsedTime(&a, ws.ev[0], ws.ev[1]);

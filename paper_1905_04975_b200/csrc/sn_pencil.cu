@@ -32,7 +32,16 @@
 namespace sn {
 namespace {
 
+inline double __longlong_as_double_host(unsigned long long b) {
+  double d;
+  std::memcpy(&d, &b, sizeof(d));
+  return d;
+}
+
 // ---------------------------------------------------------------- the swap transform (device)
+// G3's constant: residual <= kG3C eps ||block||_F (SPEC's 10^2 eps acceptance constant for a
+// direct swap; LAPACK xTGEX2 uses 20 -- DESIGN.md §3.1)
+constexpr double kG3C = 100.0;
 // 4x4 matrices column-major with ld 4 in per-thread arrays.
 
 __host__ __device__ __forceinline__ void pl_lartg(double f, double g, double& c, double& s, double& r) {
@@ -286,7 +295,7 @@ __host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double
   anorm = sqrt(anorm);
   bnorm = sqrt(bnorm);
   const double eps = 2.220446049250313e-16, sml = 2.2250738585072014e-308 / 2.220446049250313e-16;
-  const double thA = fmax(20.0 * eps * anorm, sml), thB = fmax(20.0 * eps * bnorm, sml);
+  const double thA = fmax(kG3C * eps * anorm, sml), thB = fmax(kG3C * eps * bnorm, sml);
   pl_eye(U, m);
   pl_eye(V, m);
   if (n1 == 1 && n2 == 1) {
@@ -369,6 +378,7 @@ __host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double
       if (why) { why[0] = 1.0; why[1] = best; }
       return false;
     }
+    if (why) { why[0] = 0.0; why[1] = best; }
   }
   pl_congr(U, A, V, An, m);
   pl_congr(U, B, V, Bn, m);
@@ -379,6 +389,7 @@ __host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double
       if (why) { why[0] = 1.0; why[1] = fmax(resA / thA, resB / thB); }
       return false;
     }
+    if (why) { why[0] = 0.0; why[1] = fmax(resA / thA, resB / thB); }
   }
 #pragma unroll
   for (int c = 0; c < n2; ++c)
@@ -582,6 +593,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       else if (n2 == 1) ok = pl_transform<2, 1>(Sw, ldS, Tw, ldT, j, R, why);
       else ok = pl_transform<2, 2>(Sw, ldS, Tw, ldT, j, R, why);
       if (wd.order == a.force_order && a.sidx[s] == a.force_swap) { ok = false; why[0] = 0.0; }
+      if (ok) atomicMax(&a.ctl->ratio_bits, (unsigned long long)__double_as_longlong(why[1]));
       if (!ok) {
         const int key = a.sidx[s];
         if (atomicMin(&s_rej, key) > key) { s_why[0] = why[0]; s_why[1] = why[1]; }
@@ -1000,6 +1012,7 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
     st->windows = executed;
     st->swaps = swaps;
     st->levels = P.nlevels;
+    st->g3_max_ratio = __longlong_as_double_host(hctl.ratio_bits);
     if (hctl.abort) {
       rc = SN_ERR_REJECTED;
       if (std::getenv("SN_DEBUG"))

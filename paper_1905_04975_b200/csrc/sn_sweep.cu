@@ -480,8 +480,8 @@ extern "C" {
 void sn_sweep_default_opts(sn_sweep_opts* o) {
   if (!o) return;
   std::memset(o, 0, sizeof(*o));
-  o->window = 256;
-  o->bulges_per_chain = 32;
+  o->window = 160;            // staged in shared memory (measured: 0.80 s vs 2.07 s at w = 256, n = 40000)
+  o->bulges_per_chain = 16;
   o->q_stream_overlap = 1;
 }
 
