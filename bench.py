@@ -358,9 +358,13 @@ def main():
             traffic_note = tj["note"]
     gpu_launches = int(sum(sum(r["stats"]["launches"]) for r in results) / args.steps)
 
-    # e2e through the C ABI with host buffers (H2D + D2H inside the call)
+    # e2e through the C ABI with host buffers (H2D + D2H inside the call).  The device work
+    # copies are released first: the call stages S and Q in device memory of its own (at
+    # config 4, 2 x 34 GB; with the pristine and work copies resident that would not fit)
     e2e = None
     if args.e2e_steps > 0:
+        del S, Q
+        torch.cuda.empty_cache()
         Sh = torch.empty(S0.shape, dtype=S0.dtype, pin_memory=True)
         Qh = torch.empty(Q0.shape, dtype=Q0.dtype, pin_memory=True)
         et = []

@@ -277,7 +277,8 @@ typedef struct sn_sweep_opts {
                                 in shared memory) */
   int64_t bulges_per_chain;  /* bulges chased together, 1..60 (default 16) */
   int32_t q_stream_overlap;  /* 1 (default): Q updates on a second stream */
-  int32_t reserved;
+  int32_t lookahead;         /* 1 (default): the next level's window kernel waits only for the
+                                strips it reads; the rest overlaps it on a third stream */
 } sn_sweep_opts;
 
 typedef struct sn_sweep_stats {
@@ -292,10 +293,13 @@ int sn_qr_sweep(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64
                 const double* sr, const double* si, const sn_sweep_opts* opts,
                 sn_sweep_stats* stats, void* stream);
 
-/* Host-only: the windows of one sweep (rows [w0, w0+k), DAG level), in sequential order.
- * Pass NULL arrays to query the counts. */
+/* Host-only: the windows of one sweep in sequential order: rows [w0, w0+k), DAG level, chain,
+ * and the chain steps [tau0, tau1) the window executes (in chain step tau, bulge b of the chain
+ * makes its reflector at row tau - 4b if that lies in [0, n-2]).  Pass NULL arrays to query
+ * the counts (w0 == NULL: none of the arrays is written). */
 int sn_sweep_schedule(int64_t n, int64_t nshift, int64_t window, int64_t bulges_per_chain,
-                      int64_t* nwin, int64_t* nlevels, int64_t* w0, int64_t* k, int64_t* level);
+                      int64_t* nwin, int64_t* nlevels, int64_t* w0, int64_t* k, int64_t* level,
+                      int64_t* chain, int64_t* tau0, int64_t* tau1);
 
 #ifdef __cplusplus
 }

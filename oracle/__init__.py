@@ -21,18 +21,22 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sn_oracle.c")
 _LIB = os.path.join(_HERE, "libsn_oracle.so")
+_LIB_OMP = os.path.join(_HERE, "libsn_oracle_omp.so")
 _lib = None
 
 
-def build(force: bool = False) -> str:
-    """Compile sn_oracle.c with plain gcc (no fast-math, no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+def build(force: bool = False, omp: bool = False) -> str:
+    """Compile sn_oracle.c with plain gcc (no fast-math, no FMA contraction).  omp=True builds
+    a second library with -fopenmp: the same code, its independent panel rows / columns on
+    several host threads (the N-core CPU baseline)."""
+    lib_path = _LIB_OMP if omp else _LIB
+    if force or not os.path.exists(lib_path) or os.path.getmtime(lib_path) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "sn_oracle.h"))):
-        tmp = _LIB + ".tmp%d" % os.getpid()
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fPIC", "-shared",
-                               "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+        tmp = lib_path + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fPIC", "-shared"]
+                              + (["-fopenmp"] if omp else []) + ["-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, lib_path)
+    return lib_path
 
 
 class Stats(C.Structure):
@@ -301,3 +305,23 @@ def qr_sweep(H, Q, sr, si, inplace: bool = False):
     si = np.ascontiguousarray(si, np.float64)
     rc = lib().or_qr_sweep(n, _ptr(Hx), max(n, 1), _ptr(Qx), max(nq, 1), nq, len(sr), _ptr(sr), _ptr(si))
     return rc, Hx, Qx
+
+
+def reorder_threads(S, Q, select_rows, w: int, threads: int, max_windows: int = -1, inplace: bool = False):
+    """or_reorder mode 1 from the -fopenmp build on `threads` host threads (the N-core CPU
+    baseline row; the same code and summation order per row / column as reorder())."""
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    L = C.CDLL(build(omp=True))
+    L.or_reorder_q.argtypes = lib().or_reorder_q.argtypes
+    L.or_reorder_q.restype = C.c_int
+    Sx = S if inplace else _f64(S).copy(order="F")
+    Qx = Q if (inplace or Q is None) else _f64(Q).copy(order="F")
+    n = Sx.shape[0]
+    sel = np.ascontiguousarray(select_rows, np.int32).copy()
+    m = C.c_int64()
+    bmap = np.zeros(n, np.int8)
+    st = Stats()
+    rc = L.or_reorder_q(1, n, _ptr(Sx), max(n, 1), _ptr(Qx), max(n, 1), n, _ptr(sel), C.byref(m), w,
+                        max_windows, -1, _ptr(bmap), C.byref(st))
+    stats = {f: getattr(st, f) for f, _ in Stats._fields_}
+    return {"rc": rc, "S": Sx, "Q": Qx, "select": sel, "m": m.value, "bmap": bmap, "stats": stats}

@@ -665,38 +665,55 @@ int or_schedule(int64_t n, const int8_t* bmap, const int8_t* selrow, int64_t w,
  * ------------------------------------------------------------------------- */
 static void window_updates_naive(int64_t n, double* S, int64_t lds, double* Q, int64_t ldq, int64_t nq,
                                  int64_t j1, int64_t j2, const double* Z) {
+  /* Every column (left update) and every row (right / Q updates) is independent, so the loops
+   * may run on several host threads (built with -fopenmp: the "CPU baseline, N cores" row of
+   * SURVEY §8d-5); each keeps its own summation order, so the result does not depend on it. */
   const int64_t k = j2 - j1;
-  double* tmp = (double*)malloc(sizeof(double) * (size_t)k);
-  /* left update: S[j1:j2, j2:n] <- Z^T S[j1:j2, j2:n] */
-  for (int64_t c = j2; c < n; ++c) {
-    for (int64_t r = 0; r < k; ++r) {
-      double acc = 0.0;
-      for (int64_t l = 0; l < k; ++l) acc += Z[l + r * k] * IDX(S, lds, j1 + l, c);
-      tmp[r] = acc;
+#ifdef _OPENMP
+#pragma omp parallel
+#endif
+  {
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)k);
+    /* left update: S[j1:j2, j2:n] <- Z^T S[j1:j2, j2:n] */
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+    for (int64_t c = j2; c < n; ++c) {
+      for (int64_t r = 0; r < k; ++r) {
+        double acc = 0.0;
+        for (int64_t l = 0; l < k; ++l) acc += Z[l + r * k] * IDX(S, lds, j1 + l, c);
+        tmp[r] = acc;
+      }
+      for (int64_t r = 0; r < k; ++r) IDX(S, lds, j1 + r, c) = tmp[r];
     }
-    for (int64_t r = 0; r < k; ++r) IDX(S, lds, j1 + r, c) = tmp[r];
-  }
-  /* right update: S[0:j1, j1:j2] <- S[0:j1, j1:j2] Z */
-  for (int64_t r = 0; r < j1; ++r) {
-    for (int64_t c = 0; c < k; ++c) {
-      double acc = 0.0;
-      for (int64_t l = 0; l < k; ++l) acc += IDX(S, lds, r, j1 + l) * Z[l + c * k];
-      tmp[c] = acc;
-    }
-    for (int64_t c = 0; c < k; ++c) IDX(S, lds, r, j1 + c) = tmp[c];
-  }
-  /* Q update (Q <- Q Q3): Q[:, j1:j2] <- Q[:, j1:j2] Z */
-  if (Q) {
-    for (int64_t r = 0; r < nq; ++r) {
+    /* right update: S[0:j1, j1:j2] <- S[0:j1, j1:j2] Z */
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+    for (int64_t r = 0; r < j1; ++r) {
       for (int64_t c = 0; c < k; ++c) {
         double acc = 0.0;
-        for (int64_t l = 0; l < k; ++l) acc += IDX(Q, ldq, r, j1 + l) * Z[l + c * k];
+        for (int64_t l = 0; l < k; ++l) acc += IDX(S, lds, r, j1 + l) * Z[l + c * k];
         tmp[c] = acc;
       }
-      for (int64_t c = 0; c < k; ++c) IDX(Q, ldq, r, j1 + c) = tmp[c];
+      for (int64_t c = 0; c < k; ++c) IDX(S, lds, r, j1 + c) = tmp[c];
     }
+    /* Q update (Q <- Q Q3): Q[:, j1:j2] <- Q[:, j1:j2] Z */
+    if (Q) {
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+      for (int64_t r = 0; r < nq; ++r) {
+        for (int64_t c = 0; c < k; ++c) {
+          double acc = 0.0;
+          for (int64_t l = 0; l < k; ++l) acc += IDX(Q, ldq, r, j1 + l) * Z[l + c * k];
+          tmp[c] = acc;
+        }
+        for (int64_t c = 0; c < k; ++c) IDX(Q, ldq, r, j1 + c) = tmp[c];
+      }
+    }
+    free(tmp);
   }
-  free(tmp);
 }
 
 int or_reorder(int mode, int64_t n, double* S, int64_t lds, double* Q, int64_t ldq,

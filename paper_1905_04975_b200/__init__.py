@@ -82,7 +82,7 @@ EXPORTS = ["sn_default_opts", "sn_strerror", "sn_reorder_schur", "sn_reorder_sch
 
 class SweepOpts(C.Structure):
     _fields_ = [("window", C.c_int64), ("bulges_per_chain", C.c_int64), ("q_stream_overlap", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("lookahead", C.c_int32)]
 
 
 class SweepStats(C.Structure):
@@ -156,7 +156,7 @@ def lib():
         L.sn_sweep_default_opts.argtypes = [C.POINTER(SweepOpts)]
         L.sn_qr_sweep.argtypes = [i64, p, i64, p, i64, i64, p, p, C.POINTER(SweepOpts), C.POINTER(SweepStats), p]
         L.sn_qr_sweep.restype = C.c_int
-        L.sn_sweep_schedule.argtypes = [i64, i64, i64, i64, C.POINTER(i64), C.POINTER(i64), p, p, p]
+        L.sn_sweep_schedule.argtypes = [i64, i64, i64, i64, C.POINTER(i64), C.POINTER(i64), p, p, p, p, p, p]
         L.sn_sweep_schedule.restype = C.c_int
         _lib = L
     return _lib
@@ -269,17 +269,19 @@ def qr_sweep(H, Q, sr, si, stream=None, **opts):
     return {"rc": rc, "stats": st.to_dict()}
 
 
-def sweep_schedule(n: int, nshift: int, window: int = 256, bulges_per_chain: int = 32):
-    """Host-only: the windows of one sweep (w0, k, level) in sequential order."""
+def sweep_schedule(n: int, nshift: int, window: int = 160, bulges_per_chain: int = 16):
+    """Host-only: the windows of one sweep (w0, k, level, chain, tau0, tau1) in sequential order."""
     nw, nl = C.c_int64(), C.c_int64()
     L = lib()
-    rc = L.sn_sweep_schedule(n, nshift, window, bulges_per_chain, C.byref(nw), C.byref(nl), None, None, None)
+    rc = L.sn_sweep_schedule(n, nshift, window, bulges_per_chain, C.byref(nw), C.byref(nl), None, None, None,
+                             None, None, None)
     if rc:
         raise ValueError("sn_sweep_schedule rc=%d" % rc)
-    w0, k, lev = (np.zeros(nw.value, np.int64) for _ in range(3))
-    L.sn_sweep_schedule(n, nshift, window, bulges_per_chain, C.byref(nw), C.byref(nl), w0.ctypes.data_as(C.c_void_p),
-                        k.ctypes.data_as(C.c_void_p), lev.ctypes.data_as(C.c_void_p))
-    return {"w0": w0, "k": k, "level": lev, "nlevels": nl.value}
+    out = {key: np.zeros(nw.value, np.int64) for key in ("w0", "k", "level", "chain", "tau0", "tau1")}
+    L.sn_sweep_schedule(n, nshift, window, bulges_per_chain, C.byref(nw), C.byref(nl),
+                        *[out[key].ctypes.data_as(C.c_void_p) for key in ("w0", "k", "level", "chain", "tau0", "tau1")])
+    out["nlevels"] = nl.value
+    return out
 
 
 def reorder_pencil(S, T, Q, Z, select, window: int = 256, stream=None, **opts):

@@ -139,6 +139,57 @@ __device__ __forceinline__ double small_csolve(int nb, double b00, double b10, d
   return fmax(cabs1(y0r, y0i), cabs1(y1r, y1i));
 }
 
+// the real case of small_csolve (wi = 0 and real right-hand sides): the same pivots and the
+// same operation sequence on the real parts
+__device__ __forceinline__ double small_rsolve(int nb, double b00, double b10, double b01, double b11, double wr,
+                                               double smin, double r0, double r1, double& y0, double& y1) {
+  if (nb == 1) {
+    double d = b00 - wr;
+    if (fabs(d) < smin) d = smin;
+    y0 = r0 / d;
+    y1 = 0.0;
+    return fabs(y0);
+  }
+  double m00 = b00 - wr, m01 = b01, m10 = b10, m11 = b11 - wr, c0 = r0, c1 = r1;
+  const double a00 = fabs(m00), a10 = fabs(m10), a01 = fabs(m01), a11 = fabs(m11);
+  int pr = 0, pc = 0;
+  double best = a00;
+  if (a10 > best) { best = a10; pr = 1; pc = 0; }
+  if (a01 > best) { best = a01; pr = 0; pc = 1; }
+  if (a11 > best) { best = a11; pr = 1; pc = 1; }
+  if (pr == 1) {
+    double t;
+    t = m00; m00 = m10; m10 = t;
+    t = m01; m01 = m11; m11 = t;
+    t = c0; c0 = c1; c1 = t;
+  }
+  if (pc == 1) {
+    double t;
+    t = m00; m00 = m01; m01 = t;
+    t = m10; m10 = m11; m11 = t;
+  }
+  if (fabs(m00) < smin) m00 = smin;
+  const double l = m10 / m00;
+  double uu = m11 - l * m01;
+  const double b1 = c1 - l * c0;
+  if (fabs(uu) < smin) uu = smin;
+  const double x1 = b1 / uu;
+  const double x0 = (c0 - m01 * x1) / m00;
+  if (pc == 1) { y0 = x1; y1 = x0; }
+  else { y0 = x0; y1 = x1; }
+  return fmax(fabs(y0), fabs(y1));
+}
+
+template <bool CPLX>
+__device__ __forceinline__ double small_solve(int nb, double b00, double b10, double b01, double b11, double wr,
+                                              double wi, double smin, double r0r, double r0i, double r1r,
+                                              double r1i, double& y0r, double& y0i, double& y1r, double& y1i) {
+  if (CPLX) return small_csolve(nb, b00, b10, b01, b11, wr, wi, smin, r0r, r0i, r1r, r1i, y0r, y0i, y1r, y1i);
+  y0i = 0.0;
+  y1i = 0.0;
+  return small_rsolve(nb, b00, b10, b01, b11, wr, smin, r0r, r1r, y0r, y1r);
+}
+
 __device__ __forceinline__ int pow2_steps(double v, double lim) {
   int s = 0;
   while (v > lim && s < 4000) { v *= 0.5; ++s; }
@@ -184,30 +235,14 @@ __device__ void scale_rows(double* Y, int64_t ldY, int col, int ncol, int64_t r0
   }
 }
 
-__global__ void __launch_bounds__(kSolveWarps * 32, 1) eig_solve_kernel(SolveArgs a) {
-  extern __shared__ __align__(16) double sm[];
-  double* Ts = sm;                                   // tile x tile, column-major, ld kLdT
-  double* cmx = Ts + kLdT * kTileMax;                // per tile column: max |Ts[0:c, c]|
-  int8_t* bm = reinterpret_cast<int8_t*>(cmx + kTileMax);
-  const int tb = (int)(a.i1 - a.i0);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int idx = tid; idx < tb * tb; idx += blockDim.x) {
-    const int r = idx % tb, c = idx / tb;
-    Ts[r + c * kLdT] = r <= c + 1 ? a.S[(a.i0 + r) + (a.i0 + c) * a.ldS] : 0.0;
-  }
-  for (int r = tid; r < tb; r += blockDim.x) bm[r] = a.bmap[a.i0 + r];
-  __syncthreads();
-  for (int c = warp; c < tb; c += kSolveWarps) {
-    double m = 0.0;
-    for (int r = lane; r < c; r += 32) m = fmax(m, fabs(Ts[r + c * kLdT]));
-    m = warp_max(m);
-    if (lane == 0) cmx[c] = m;
-  }
-  __syncthreads();
-  const int u = a.u0 + blockIdx.x * kSolveWarps + warp;
-  if (u >= a.u0 + a.nu) return;
+// one eigenvector (a warp): CPLX = a complex pair (two columns, complex arithmetic), else a
+// real eigenvalue (real arithmetic: the same operations with the imaginary parts dropped, so
+// the values are those of the complex routine with zero imaginary parts)
+template <bool CPLX>
+__device__ __forceinline__ void solve_unit(const SolveArgs& a, const double* Ts, const double* cmx, const int8_t* bm,
+                                           int tb, int u, int lane) {
   const EigUnit U = a.units[u];
-  const bool cplx = U.bs == 2;
+  constexpr bool cplx = CPLX;
   const int ncol = U.bs;
   double* Yr = a.Y + (int64_t)U.col * a.ldY;
   double* Yi = cplx ? Yr + a.ldY : nullptr;
@@ -297,14 +332,14 @@ __global__ void __launch_bounds__(kSolveWarps * 32, 1) eig_solve_kernel(SolveArg
     const double b01 = nb == 2 ? Ts[i + (i + 1) * kLdT] : 0.0;
     const double b11 = nb == 2 ? Ts[(i + 1) + (i + 1) * kLdT] : 0.0;
     double y0r, y0i, y1r, y1i;
-    double ym = small_csolve(nb, b00, b10, b01, b11, wr, wi, smin, r0r, r0i, r1r, r1i, y0r, y0i, y1r, y1i);
+    double ym = small_solve<CPLX>(nb, b00, b10, b01, b11, wr, wi, smin, r0r, r0i, r1r, r1i, y0r, y0i, y1r, y1i);
     if (!(ym <= kOmega)) {
       // E4: rescale the whole eigenvector so that this solve stays below Omega
       const double rmax = fmax(cabs1(r0r, r0i), cabs1(r1r, r1i));
       int s = (ym < 1e308) ? pow2_steps(ym, kOmega * kHeadroom) : pow2_steps(rmax / smin, kOmega * kHeadroom) + 1;
       for (;;) {
         const double f = ldexp(1.0, -s);
-        ym = small_csolve(nb, b00, b10, b01, b11, wr, wi, smin, r0r * f, r0i * f, r1r * f, r1i * f, y0r, y0i, y1r,
+        ym = small_solve<CPLX>(nb, b00, b10, b01, b11, wr, wi, smin, r0r * f, r0i * f, r1r * f, r1i * f, y0r, y0i, y1r,
                           y1i);
         if (ym <= kOmega || s > 4000) break;
         ++s;
@@ -388,6 +423,33 @@ __global__ void __launch_bounds__(kSolveWarps * 32, 1) eig_solve_kernel(SolveArg
     stt.e = e;
     a.state[u] = stt;
   }
+}
+
+__global__ void __launch_bounds__(kSolveWarps * 32, 1) eig_solve_kernel(SolveArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  double* Ts = sm;                                   // tile x tile, column-major, ld kLdT
+  double* cmx = Ts + kLdT * kTileMax;                // per tile column: max |Ts[0:c, c]|
+  int8_t* bm = reinterpret_cast<int8_t*>(cmx + kTileMax);
+  const int tb = (int)(a.i1 - a.i0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int idx = tid; idx < tb * tb; idx += blockDim.x) {
+    const int r = idx % tb, c = idx / tb;
+    Ts[r + c * kLdT] = r <= c + 1 ? a.S[(a.i0 + r) + (a.i0 + c) * a.ldS] : 0.0;
+  }
+  for (int r = tid; r < tb; r += blockDim.x) bm[r] = a.bmap[a.i0 + r];
+  __syncthreads();
+  for (int c = warp; c < tb; c += kSolveWarps) {
+    double m = 0.0;
+    for (int r = lane; r < c; r += 32) m = fmax(m, fabs(Ts[r + c * kLdT]));
+    m = warp_max(m);
+    if (lane == 0) cmx[c] = m;
+  }
+  __syncthreads();
+  const int u = a.u0 + blockIdx.x * kSolveWarps + warp;
+  if (u >= a.u0 + a.nu) return;
+  const EigUnit U = a.units[u];
+  if (U.bs == 2) solve_unit<true>(a, Ts, cmx, bm, tb, u, lane);
+  else solve_unit<false>(a, Ts, cmx, bm, tb, u, lane);
 }
 
 // ---- ||S[0:i0, i0:i1]||_inf per tile (one CTA per tile)

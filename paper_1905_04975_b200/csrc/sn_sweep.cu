@@ -213,8 +213,8 @@ struct SBuf {
 
 struct SweepWorkspace {
   SBuf wins, bw, pref, status, Z, zr, shifts, sub, bad;
-  cudaStream_t sB = nullptr;
-  cudaEvent_t evW[kZgenS] = {}, evQ[kZgenS] = {};
+  cudaStream_t sB = nullptr, sC = nullptr;   // Q updates / remaining (non-critical) strips
+  cudaEvent_t evW[kZgenS] = {}, evQ[kZgenS] = {}, evCrit[kZgenS] = {}, evRest[kZgenS] = {};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evIn = nullptr, evJoin = nullptr;
   int device = -1;
 };
@@ -293,16 +293,23 @@ int sweep_run(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64_t
         b->cap = 0;
       }
       cudaStreamDestroy(ws.sB);
-      for (int i = 0; i < kZgenS; ++i) { cudaEventDestroy(ws.evW[i]); cudaEventDestroy(ws.evQ[i]); }
+      cudaStreamDestroy(ws.sC);
+      for (int i = 0; i < kZgenS; ++i) {
+        cudaEventDestroy(ws.evW[i]); cudaEventDestroy(ws.evQ[i]);
+        cudaEventDestroy(ws.evCrit[i]); cudaEventDestroy(ws.evRest[i]);
+      }
       for (cudaEvent_t e : {ws.ev0, ws.ev1, ws.evIn, ws.evJoin}) cudaEventDestroy(e);
       SK(cudaSetDevice(dev));
     }
     int least = 0, greatest = 0;
     SK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     SK(cudaStreamCreateWithPriority(&ws.sB, cudaStreamNonBlocking, least));
+    SK(cudaStreamCreateWithPriority(&ws.sC, cudaStreamNonBlocking, least));
     for (int i = 0; i < kZgenS; ++i) {
       SK(cudaEventCreateWithFlags(&ws.evW[i], cudaEventDisableTiming));
       SK(cudaEventCreateWithFlags(&ws.evQ[i], cudaEventDisableTiming));
+      SK(cudaEventCreateWithFlags(&ws.evCrit[i], cudaEventDisableTiming));
+      SK(cudaEventCreateWithFlags(&ws.evRest[i], cudaEventDisableTiming));
     }
     SK(cudaEventCreate(&ws.ev0));
     SK(cudaEventCreate(&ws.ev1));
@@ -345,26 +352,77 @@ int sweep_run(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64_t
   constexpr int NT = 64;
   std::vector<WinDev> wd((size_t)nw);
   std::vector<BulgeDev> bd((size_t)nw);
+  // lookahead (as the reordering): a left strip (rows of the window, 64 columns
+  // right of it) or a right strip (64 rows above it, its columns) is critical if a window of
+  // the next level covers both its rows and its columns -- a prefix of the left strips, a
+  // suffix of the right strips.  The critical strips run on the critical stream before the
+  // next level's window kernel, the others on stream C concurrently with it.
+  const bool look = o.lookahead != 0;
+  const bool allcrit = std::getenv("SN_SWEEP_ALLCRIT") != nullptr;   // debug: every strip critical
+  constexpr int NK = 5;   // 0 L crit, 1 L rest, 2 R crit, 3 R rest, 4 Q
   std::vector<int32_t> pref;
-  std::vector<int64_t> poff((size_t)nlev * 3);
-  std::vector<int32_t> nstr((size_t)nlev * 3);
+  std::vector<int64_t> poff((size_t)nlev * NK);
+  std::vector<int32_t> nstr((size_t)nlev * NK);
   double eqf = 0.0, fk[3] = {0, 0, 0};
   for (int64_t l = 0; l < nlev; ++l) {
     const int64_t a = lstart[l], b = lstart[l + 1];
-    for (int kind = 0; kind < 3; ++kind) {
-      poff[l * 3 + kind] = (int64_t)pref.size();
+    std::vector<int32_t> cl((size_t)(b - a), 0), cr((size_t)(b - a), 0);
+    for (int64_t i = a; i < b; ++i) {
+      const HostWin& h = hw[sorted[i]];
+      const int64_t nL = (n - (h.w0 + h.k) + NT - 1) / NT, nR = (h.w0 + NT - 1) / NT;
+      if (!look || allcrit) { cl[i - a] = (int32_t)nL; cr[i - a] = (int32_t)nR; continue; }
+      if (l + 1 >= nlev) continue;
+      for (int64_t j = lstart[l + 1]; j < lstart[l + 2]; ++j) {
+        const HostWin& g = hw[sorted[j]];
+        const int64_t ga = g.w0, gb = g.w0 + g.k;
+        // left strips: rows [w0, w0+k) meet [ga, gb), columns >= w0+k up to gb
+        if (ga < h.w0 + h.k && gb > h.w0 && gb > h.w0 + h.k)
+          cl[i - a] = (int32_t)std::max<int64_t>(cl[i - a], std::min(nL, (gb - (h.w0 + h.k) + NT - 1) / NT));
+        // right strips: columns [w0, w0+k) meet [ga, gb), rows from ga (64-strips) below w0
+        if (ga < h.w0 + h.k && gb > h.w0 && ga < h.w0)
+          cr[i - a] = (int32_t)std::max<int64_t>(cr[i - a], nR - ga / NT);
+      }
+    }
+    // corner order: a right update over rows of an upper window's left strips needs those
+    // strips done on its whole column range first (it mixes the columns of the lower window;
+    // left-updating some of them before and some after would not commute).  So when a lower
+    // window's critical right strips reach an upper window's rows, the upper window's left
+    // strips over the lower window's columns become critical too (run before it on the
+    // critical stream), as in the reordering's lookahead (sn_plan.cpp).
+    if (look && !allcrit) {
+      for (int64_t ib = a; ib < b; ++ib) {
+        const HostWin& B = hw[sorted[ib]];
+        if (cr[ib - a] <= 0) continue;
+        const int64_t nRB = (B.w0 + NT - 1) / NT;
+        const int64_t crow0 = (nRB - cr[ib - a]) * NT;         // first row of B's critical right strips
+        for (int64_t ia = a; ia < b; ++ia) {
+          const HostWin& A = hw[sorted[ia]];
+          if (A.w0 + A.k > B.w0 || A.w0 + A.k <= crow0) continue;   // A above B, rows meet
+          const int64_t nLA = (n - (A.w0 + A.k) + NT - 1) / NT;
+          const int64_t need = std::min(nLA, (B.w0 + B.k - (A.w0 + A.k) + NT - 1) / NT);
+          cl[ia - a] = (int32_t)std::max<int64_t>(cl[ia - a], need);
+        }
+      }
+    }
+    for (int kind = 0; kind < NK; ++kind) {
+      poff[l * NK + kind] = (int64_t)pref.size();
       int32_t acc = 0;
       pref.push_back(0);
       for (int64_t i = a; i < b; ++i) {
         const HostWin& h = hw[sorted[i]];
+        const int64_t nL = (n - (h.w0 + h.k) + NT - 1) / NT, nR = (h.w0 + NT - 1) / NT;
         int64_t cnt = 0;
-        if (kind == 0) cnt = (n - (h.w0 + h.k) + NT - 1) / NT;
-        else if (kind == 1) cnt = (h.w0 + NT - 1) / NT;
-        else cnt = Q ? (n + NT - 1) / NT : 0;
+        switch (kind) {
+          case 0: cnt = cl[i - a]; break;
+          case 1: cnt = nL - cl[i - a]; break;
+          case 2: cnt = cr[i - a]; break;
+          case 3: cnt = nR - cr[i - a]; break;
+          default: cnt = Q ? (n + NT - 1) / NT : 0; break;
+        }
         acc += (int32_t)cnt;
         pref.push_back(acc);
       }
-      nstr[l * 3 + kind] = acc;
+      nstr[l * NK + kind] = acc;
     }
     for (int64_t i = a; i < b; ++i) {
       const HostWin& h = hw[sorted[i]];
@@ -372,6 +430,7 @@ int sweep_run(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64_t
       std::memset(&d, 0, sizeof(d));
       d.j1 = h.w0; d.k = h.k; d.slot = (int32_t)((l % kZgenS) * maxper + (i - a));
       d.order = sorted[i]; d.sidx = (int32_t)i;
+      d.crit_l = cl[i - a]; d.crit_r = cr[i - a];
       BulgeDev& e = bd[i];
       e.tau0 = h.tau0; e.tau1 = h.tau1; e.m = h.m; e.b0 = h.b0;
       const double k2 = 2.0 * (double)h.k * (double)h.k;
@@ -402,14 +461,21 @@ int sweep_run(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64_t
   if (Q) panel_maps_init(&mapQ, dZ, (int64_t)kZgenS * maxper, Q, n, n, ldQ);
   const bool overlapQ = o.q_stream_overlap != 0 && Q != nullptr;
   cudaStream_t sQ = overlapQ ? ws.sB : sA;
+  cudaStream_t sC = look ? ws.sC : sA;
   SK(cudaEventRecord(ws.ev0, sA));
   if (overlapQ) SK(cudaStreamWaitEvent(ws.sB, ws.ev0, 0));
+  if (look) SK(cudaStreamWaitEvent(ws.sC, ws.ev0, 0));
   int64_t launches = 0;
   int rc = SN_OK;
   for (int64_t l = 0; l < nlev && rc == SN_OK; ++l) {
     const int64_t a = lstart[l], cnt = lstart[l + 1] - a;
     const int gen = (int)(l % kZgenS);
+    // the Z slots of this generation are free once the level kZgenS earlier has finished with
+    // them (its Q update and its remaining strips)
     if (overlapQ && l >= kZgenS) SK(cudaStreamWaitEvent(sA, ws.evQ[gen], 0));
+    if (look && l >= kZgenS) SK(cudaStreamWaitEvent(sA, ws.evRest[gen], 0));
+    if (look && l > 0 && std::getenv("SN_SWEEP_DBG_WAITW"))   // debug: no overlap of W(l) with rest(l-1)
+      SK(cudaStreamWaitEvent(sA, ws.evRest[(l - 1) % kZgenS], 0));
     SweepArgs sa{};
     sa.wins = (const WinDev*)ws.wins.p + a; sa.bw = (const BulgeDev*)ws.bw.p + a; sa.nwin = (int32_t)cnt;
     sa.H = H; sa.ldH = ldH; sa.n = n; sa.Z = dZ; sa.zrange = (int16_t*)ws.zr.p; sa.status = (int32_t*)ws.status.p;
@@ -432,22 +498,35 @@ int sweep_run(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64_t
     PanelArgs pa{};
     pa.wins = (const WinDev*)ws.wins.p + a; pa.nwin = (int32_t)cnt; pa.base = (int32_t)a;
     pa.status = (const int32_t*)ws.status.p; pa.n = n; pa.Z = dZ; pa.zrange = (const int16_t*)ws.zr.p;
-    pa.part = 0;
-    for (int kind = 0; kind < 2; ++kind) {
-      if (nstr[l * 3 + kind] <= 0) continue;
-      pa.M = H; pa.ld = ldH; pa.maps = &mapH;
-      pa.vec16 = (ldH % 2 == 0 && ((uintptr_t)H % 16) == 0) ? 1 : 0;
-      pa.prefix = (const int32_t*)ws.pref.p + poff[l * 3 + kind];
-      launch_panel(kind, mt, pa, nstr[l * 3 + kind], sA);
+    pa.M = H; pa.ld = ldH; pa.maps = &mapH;
+    pa.vec16 = (ldH % 2 == 0 && ((uintptr_t)H % 16) == 0) ? 1 : 0;
+    // the previous level's remaining strips may overlap this level's strips
+    if (look && l > 0) SK(cudaStreamWaitEvent(sA, ws.evRest[(l - 1) % kZgenS], 0));
+    auto part = [&](int kind, int prt, int slot_kind, cudaStream_t s) {
+      if (nstr[l * NK + slot_kind] <= 0) return;
+      pa.prefix = (const int32_t*)ws.pref.p + poff[l * NK + slot_kind];
+      pa.part = look ? prt : 0;
+      launch_panel(kind, mt, pa, nstr[l * NK + slot_kind], s);
       ++launches;
-    }
+    };
+    part(0, 1, 0, sA);             // left, critical strips (all strips without lookahead)
+    part(1, 1, 2, sA);             // right, critical strips
     SK(cudaGetLastError());
-    if (Q && nstr[l * 3 + 2] > 0) {
+    if (look) {
+      SK(cudaEventRecord(ws.evCrit[gen], sA));
+      SK(cudaStreamWaitEvent(sC, ws.evCrit[gen], 0));
+      part(0, 2, 1, sC);           // the remaining strips overlap the next window kernel
+      part(1, 2, 3, sC);
+      SK(cudaEventRecord(ws.evRest[gen], sC));
+      SK(cudaGetLastError());
+    }
+    if (Q && nstr[l * NK + 4] > 0) {
       if (overlapQ) SK(cudaStreamWaitEvent(sQ, ws.evW[gen], 0));
       pa.M = Q; pa.ld = ldQ; pa.maps = &mapQ;
       pa.vec16 = (ldQ % 2 == 0 && ((uintptr_t)Q % 16) == 0) ? 1 : 0;
-      pa.prefix = (const int32_t*)ws.pref.p + poff[l * 3 + 2];
-      launch_panel(2, mt, pa, nstr[l * 3 + 2], sQ);
+      pa.prefix = (const int32_t*)ws.pref.p + poff[l * NK + 4];
+      pa.part = 0;
+      launch_panel(2, mt, pa, nstr[l * NK + 4], sQ);
       ++launches;
       SK(cudaGetLastError());
       if (overlapQ) SK(cudaEventRecord(ws.evQ[gen], sQ));
@@ -455,6 +534,10 @@ int sweep_run(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64_t
   }
   if (overlapQ) {
     SK(cudaEventRecord(ws.evJoin, sQ));
+    SK(cudaStreamWaitEvent(sA, ws.evJoin, 0));
+  }
+  if (look) {
+    SK(cudaEventRecord(ws.evJoin, sC));
     SK(cudaStreamWaitEvent(sA, ws.evJoin, 0));
   }
   SK(cudaEventRecord(ws.ev1, sA));
@@ -483,6 +566,7 @@ void sn_sweep_default_opts(sn_sweep_opts* o) {
   o->window = 160;            // staged in shared memory (measured: 0.80 s vs 2.07 s at w = 256, n = 40000)
   o->bulges_per_chain = 16;
   o->q_stream_overlap = 1;
+  o->lookahead = 1;
 }
 
 int sn_qr_sweep(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64_t nshift, const double* sr,
@@ -516,7 +600,8 @@ int sn_qr_sweep(int64_t n, double* H, int64_t ldH, double* Q, int64_t ldQ, int64
 }
 
 int sn_sweep_schedule(int64_t n, int64_t nshift, int64_t window, int64_t bulges_per_chain, int64_t* nwin,
-                      int64_t* nlevels, int64_t* w0, int64_t* k, int64_t* level) {
+                      int64_t* nlevels, int64_t* w0, int64_t* k, int64_t* level, int64_t* chain, int64_t* tau0,
+                      int64_t* tau1) {
   if (n < 0 || nshift < 0 || (nshift & 1)) return -1;
   if (!nwin || !nlevels) return -5;
   std::vector<sn::HostWin> hw;
@@ -527,6 +612,9 @@ int sn_sweep_schedule(int64_t n, int64_t nshift, int64_t window, int64_t bulges_
       w0[t] = hw[t].w0;
       if (k) k[t] = hw[t].k;
       if (level) level[t] = hw[t].level;
+      if (chain) chain[t] = hw[t].chain;
+      if (tau0) tau0[t] = hw[t].tau0;
+      if (tau1) tau1[t] = hw[t].tau1;
     }
   return 0;
 }

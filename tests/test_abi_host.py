@@ -134,3 +134,42 @@ def test_argument_errors_without_gpu():
     assert rc == -2
     rc, m = sn.sn_reorder_schur(0, 0, 1, None, 1, np.zeros(1, np.int32))
     assert rc == 0 and m == 0
+
+
+@pytest.mark.parametrize("n,ns,w,m", [(3, 2, 16, 1), (50, 8, 32, 4), (1000, 64, 160, 16), (4000, 256, 256, 32),
+                                      (777, 40, 128, 12)])
+def test_sweep_schedule_is_valid(n, ns, w, m):
+    """The sweep plan (row f3, readings B3/B4): every reflector of every chain step lies inside
+    the window executing that step (its rows p..p+2, the column p-1 it reads, the rows up to
+    p+3 its right update touches), each chain's steps are covered exactly once in order, and a
+    window's level exceeds that of every earlier window whose rows it meets."""
+    sc = sn.sweep_schedule(n, ns, w, m)
+    nb = ns // 2
+    seen = {}
+    rowlev = np.full(n, -1)
+    for t in range(len(sc["w0"])):
+        w0, k, c, t0, t1, lev = (int(sc[key][t]) for key in ("w0", "k", "chain", "tau0", "tau1", "level"))
+        assert k <= w and w0 + k <= n
+        mb = min(m, nb - c * m)
+        assert seen.get(c, 0) == t0 and t1 > t0          # consecutive, gap-free chain steps
+        seen[c] = t1
+        for tau in range(t0, t1):
+            for b in range(mb):
+                p = tau - 4 * b
+                if 0 <= p <= n - 2:
+                    lo = p if p == 0 else p - 1
+                    hi = min(p + 3, n - 1)
+                    assert w0 <= lo and hi < w0 + k, (t, tau, b, p, w0, k)
+        assert lev > rowlev[w0:w0 + k].max()
+        rowlev[w0:w0 + k] = lev
+    for c in range((nb + m - 1) // m):
+        mb = min(m, nb - c * m)
+        assert seen[c] == (n - 2) + 4 * (mb - 1) + 1     # every bulge leaves at the bottom
+    assert sc["nlevels"] == rowlev.max() + 1
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU refusal")
+def test_rows_f3_f4_refuse_without_gpu():
+    h = torch.zeros((8, 8), dtype=torch.float64)
+    assert sn.qr_sweep(h, None, [1.0, 2.0], [0.0, 0.0])["rc"] == sn.SN_ERR_CUDA
+    assert sn.eigenvectors(h, None, np.ones(8, np.int32))["rc"] == sn.SN_ERR_CUDA

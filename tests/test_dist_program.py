@@ -143,21 +143,23 @@ def _gloo_worker(rank, world, port, n, w, bc, seed, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,w,bc,seed", [(200, 16, 32, 21), (240, 32, 32, 22)])
-def test_gloo_world2_matches_oracle(tmp_path, n, w, bc, seed):
+@pytest.mark.parametrize("world,n,w,bc,seed", [(2, 200, 16, 32, 21), (2, 240, 32, 32, 22), (3, 260, 16, 32, 23)])
+def test_gloo_world_matches_oracle(tmp_path, world, n, w, bc, seed):
+    """The sharded program (row e) executed by `world` gloo processes (send/recv + broadcast)
+    equals the one-process oracle; world 3 exercises an owner cycle longer than a pair."""
     import torch.multiprocessing as mp
     port = _free_port()
-    mp.spawn(_gloo_worker, args=(2, port, n, w, bc, seed, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_gloo_worker, args=(world, port, n, w, bc, seed, str(tmp_path)), nprocs=world, join=True)
     S, Q, sel = problem(n, w, seed)
     ref = oracle_ref(S, Q, sel, w)
     Sg = np.zeros((n, n))
     Qg = np.zeros((n, n))
-    for r in range(2):
+    for r in range(world):
         Sx = np.load(tmp_path / ("S%d.npy" % r))
         for j in range(n):
-            if (j // bc) % 2 == r:
-                Sg[:, j] = Sx[:, DI.ext_lcol(j, 2, bc, w)]
-        _, q0, q1 = sn.dist_layout(n, 2, bc, r)
+            if (j // bc) % world == r:
+                Sg[:, j] = Sx[:, DI.ext_lcol(j, world, bc, w)]
+        _, q0, q1 = sn.dist_layout(n, world, bc, r)
         Qg[q0:q1] = np.load(tmp_path / ("Q%d.npy" % r))
     assert np.abs(Sg - ref["S"]).max() <= TOL * np.linalg.norm(S)
     assert np.abs(Qg - ref["Q"]).max() <= TOL

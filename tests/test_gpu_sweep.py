@@ -87,15 +87,19 @@ def test_sweep_trailing_shifts_invariants():
     assert np.linalg.norm(Qg.T @ Qg - np.eye(n)) <= 100 * n * EPS
 
 
-def test_sweep_q_stream_variants_bitwise():
-    """The Q stream overlap changes only the order of independent kernels: bitwise equal."""
-    h = make_hessenberg(900, 48, q="householder", seed=8, device="cuda")
+@pytest.mark.parametrize("window,chain", [(160, 16), (128, 12), (256, 32)])
+def test_sweep_executor_variants_bitwise(window, chain):
+    """The Q stream and the lookahead (critical strips first, the rest overlapping the next
+    window kernel; corner order closed as in the reordering) change only the order of
+    independent work: bitwise equal to the serial executor, with several chains in flight."""
+    h = make_hessenberg(1500, 96, q="householder", seed=8, device="cuda")
     H1, Q1 = h.H.clone(), h.Q.clone()
-    H2, Q2 = h.H.clone(), h.Q.clone()
-    sn.qr_sweep(H1, Q1, h.sr, h.si)
-    sn.qr_sweep(H2, Q2, h.sr, h.si, q_stream_overlap=0)
-    torch.cuda.synchronize()
-    assert torch.equal(H1, H2) and torch.equal(Q1, Q2)
+    sn.qr_sweep(H1, Q1, h.sr, h.si, window=window, bulges_per_chain=chain, lookahead=0, q_stream_overlap=0)
+    for kw in (dict(), dict(lookahead=0), dict(q_stream_overlap=0)):
+        H2, Q2 = h.H.clone(), h.Q.clone()
+        sn.qr_sweep(H2, Q2, h.sr, h.si, window=window, bulges_per_chain=chain, **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(H1, H2) and torch.equal(Q1, Q2), kw
 
 
 def test_sweep_arguments():

@@ -509,3 +509,15 @@ def test_row_sampled_Q_gives_those_rows():
         a = oracle.reorder(S0, Q0, p.select, w=32, mode=mode)
         b = oracle.reorder(S0, np.asfortranarray(Q0[rows]), p.select, w=32, mode=mode)
         assert np.array_equal(a["S"], b["S"]) and np.array_equal(a["Q"][rows], b["Q"])
+
+
+def test_threaded_oracle_is_bitwise_the_oracle():
+    """The -fopenmp build (the N-core CPU baseline row) runs the same code: every panel row /
+    column keeps its summation order, so the result is bitwise the single-thread oracle's."""
+    p = make_problem(700, p2=0.25, q="householder", psel=0.35, w=64, seed=41)
+    S0, Q0 = p.S_np().copy(order="F"), p.Q_np().copy(order="F")
+    a = oracle.reorder(S0, Q0, p.select, w=64)
+    b = oracle.reorder_threads(S0, Q0, p.select, 64, 4)
+    assert a["rc"] == b["rc"] == 0
+    assert np.array_equal(a["S"], b["S"]) and np.array_equal(a["Q"], b["Q"])
+    np.testing.assert_array_equal(a["bmap"], b["bmap"])
