@@ -40,12 +40,16 @@ constexpr double kOmega = 3.273390607896142e+150;   // 2^500 (E4)
 // result is the same (power-of-two scalings) up to entries below 2^-674 of the vector's
 // largest one, which may underflow to zero -- far below any comparison bar
 constexpr double kHeadroom = 1.18575755001e-271;   // 2^-900
-constexpr int kTileRows = 128;                        // nominal row tile (<= 129 with a 2x2 shift)
-constexpr int kTileMax = 130;
+// Row tiles of 64 rows: the per-step dependency chain of the solve touches 3 registers per lane
+// (not 5), the kernel fits 2 CTAs (32 warps) per SM, and the update GEMMs keep a long K loop
+// through the super-tiles (8 tiles, K ~ 512).
+constexpr int kTileRows = 64;                         // nominal row tile (<= 65 with a 2x2 shift)
+constexpr int kTileMax = 66;
 constexpr int kLdT = kTileMax + 1;                    // odd stride of the staged diagonal tile
-constexpr int kRegs = 5;                              // rows per lane: 5 x 32 >= kTileMax
-constexpr int kSolveWarps = 16;
-constexpr int kSuper = 4;                             // row tiles per update super-tile
+constexpr int kRegs = 3;                              // rows per lane: 3 x 32 >= kTileMax
+constexpr int kSolveWarps = 12;
+constexpr int kSolveCtasPerSm = 2;
+constexpr int kSuper = 8;                             // row tiles per update super-tile
 
 struct EigUnit {
   int64_t k;      // first row of the eigenvalue's block
@@ -425,7 +429,7 @@ __device__ __forceinline__ void solve_unit(const SolveArgs& a, const double* Ts,
   }
 }
 
-__global__ void __launch_bounds__(kSolveWarps * 32, 1) eig_solve_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(kSolveWarps * 32, kSolveCtasPerSm) eig_solve_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double sm[];
   double* Ts = sm;                                   // tile x tile, column-major, ld kLdT
   double* cmx = Ts + kLdT * kTileMax;                // per tile column: max |Ts[0:c, c]|
