@@ -1,6 +1,7 @@
 // sn_device.cuh -- device-side data layout shared by the executor and the kernels.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 

@@ -40,16 +40,15 @@ constexpr double kOmega = 3.273390607896142e+150;   // 2^500 (E4)
 // result is the same (power-of-two scalings) up to entries below 2^-674 of the vector's
 // largest one, which may underflow to zero -- far below any comparison bar
 constexpr double kHeadroom = 1.18575755001e-271;   // 2^-900
-// Row tiles of 64 rows: the per-step dependency chain of the solve touches 3 registers per lane
-// (not 5), the kernel fits 2 CTAs (32 warps) per SM, and the update GEMMs keep a long K loop
-// through the super-tiles (8 tiles, K ~ 512).
-constexpr int kTileRows = 64;                         // nominal row tile (<= 65 with a 2x2 shift)
-constexpr int kTileMax = 66;
+// Row tiles of 128 rows (64-row tiles were measured slower: 0.62 s of solves instead of 0.46 s
+// at config 3 -- twice the launches, the same serial chain length per eigenvector)
+constexpr int kTileRows = 128;                        // nominal row tile (<= 129 with a 2x2 shift)
+constexpr int kTileMax = 130;
 constexpr int kLdT = kTileMax + 1;                    // odd stride of the staged diagonal tile
-constexpr int kRegs = 3;                              // rows per lane: 3 x 32 >= kTileMax
-constexpr int kSolveWarps = 12;
-constexpr int kSolveCtasPerSm = 2;
-constexpr int kSuper = 8;                             // row tiles per update super-tile
+constexpr int kRegs = 5;                              // rows per lane: 5 x 32 >= kTileMax
+constexpr int kSolveWarps = 16;
+constexpr int kSolveCtasPerSm = 1;
+constexpr int kSuper = 4;                             // row tiles per update super-tile
 
 struct EigUnit {
   int64_t k;      // first row of the eigenvalue's block
