@@ -318,84 +318,121 @@ __device__ __forceinline__ void solve_unit(const SolveArgs& a, const double* Ts,
   B = warp_max(B);
   // rows of the unit below the tile part solved here (global): [i0 + rend, k + bs)
   const int64_t below0 = a.i0 + rend, below1 = U.k + U.bs;
+  // Rows solved bottom to top, in phases J = kRegs-1 .. 0 of 32 rows: register J of lane l
+  // holds row 32J + l, so inside a phase the register index is a compile-time constant (no
+  // runtime register selection), and a solved block updates register J (lanes above it) and
+  // the lower registers.  A 2x2 block whose rows straddle two phases belongs to the lower
+  // phase (its first row), its second row read from / written to register J+1, lane 0.
   int i = rend;
-  while (i > 0) {
-    const int nb = (i >= 2 && bm[i - 1] == 2) ? 2 : 1;
-    i -= nb;
-    const int j0 = i >> 5, l0 = i & 31, j1 = (i + 1) >> 5, l1 = (i + 1) & 31;
-    double r0r = __shfl_sync(0xffffffffu, reg_get(vr, j0), l0);
-    double r0i = __shfl_sync(0xffffffffu, reg_get(vi, j0), l0);
-    double r1r = 0.0, r1i = 0.0;
-    if (nb == 2) {
-      r1r = __shfl_sync(0xffffffffu, reg_get(vr, j1), l1);
-      r1i = __shfl_sync(0xffffffffu, reg_get(vi, j1), l1);
-    }
-    const double b00 = Ts[i + i * kLdT];
-    const double b10 = nb == 2 ? Ts[(i + 1) + i * kLdT] : 0.0;
-    const double b01 = nb == 2 ? Ts[i + (i + 1) * kLdT] : 0.0;
-    const double b11 = nb == 2 ? Ts[(i + 1) + (i + 1) * kLdT] : 0.0;
-    double y0r, y0i, y1r, y1i;
-    double ym = small_solve<CPLX>(nb, b00, b10, b01, b11, wr, wi, smin, r0r, r0i, r1r, r1i, y0r, y0i, y1r, y1i);
-    if (!(ym <= kOmega)) {
-      // E4: rescale the whole eigenvector so that this solve stays below Omega
-      const double rmax = fmax(cabs1(r0r, r0i), cabs1(r1r, r1i));
-      int s = (ym < 1e308) ? pow2_steps(ym, kOmega * kHeadroom) : pow2_steps(rmax / smin, kOmega * kHeadroom) + 1;
-      for (;;) {
-        const double f = ldexp(1.0, -s);
-        ym = small_solve<CPLX>(nb, b00, b10, b01, b11, wr, wi, smin, r0r * f, r0i * f, r1r * f, r1i * f, y0r, y0i, y1r,
-                          y1i);
-        if (ym <= kOmega || s > 4000) break;
-        ++s;
+#pragma unroll
+  for (int J = kRegs - 1; J >= 0; --J) {
+    while (i > 32 * J) {
+      const int nb = (i >= 2 && bm[i - 1] == 2) ? 2 : 1;
+      if (i - nb < 32 * J) break;            // a straddling 2x2 block: the next phase's
+      i -= nb;
+      const int l0 = i - 32 * J;             // lane of the block's first row
+      const bool up = (nb == 2 && l0 == 31); // its second row in register J+1, lane 0
+      double r0r = __shfl_sync(0xffffffffu, vr[J], l0);
+      double r0i = CPLX ? __shfl_sync(0xffffffffu, vi[J], l0) : 0.0;
+      double r1r = 0.0, r1i = 0.0;
+      if (nb == 2) {
+        const double nr = (J + 1 < kRegs) ? vr[J + 1 < kRegs ? J + 1 : J] : 0.0;
+        const double ni = (J + 1 < kRegs) ? vi[J + 1 < kRegs ? J + 1 : J] : 0.0;
+        const double sr = up ? nr : vr[J];
+        const double si2 = up ? ni : vi[J];
+        r1r = __shfl_sync(0xffffffffu, sr, up ? 0 : l0 + 1);
+        r1i = CPLX ? __shfl_sync(0xffffffffu, si2, up ? 0 : l0 + 1) : 0.0;
       }
-      const double f = ldexp(1.0, -s);
+      const double b00 = Ts[i + i * kLdT];
+      const double b10 = nb == 2 ? Ts[(i + 1) + i * kLdT] : 0.0;
+      const double b01 = nb == 2 ? Ts[i + (i + 1) * kLdT] : 0.0;
+      const double b11 = nb == 2 ? Ts[(i + 1) + (i + 1) * kLdT] : 0.0;
+      double y0r, y0i, y1r, y1i;
+      double ym = small_solve<CPLX>(nb, b00, b10, b01, b11, wr, wi, smin, r0r, r0i, r1r, r1i, y0r, y0i, y1r, y1i);
+      if (!(ym <= kOmega)) {
+        // E4: rescale the whole eigenvector so that this solve stays below Omega
+        const double rmax = fmax(cabs1(r0r, r0i), cabs1(r1r, r1i));
+        int s = (ym < 1e308) ? pow2_steps(ym, kOmega * kHeadroom) : pow2_steps(rmax / smin, kOmega * kHeadroom) + 1;
+        for (;;) {
+          const double f = ldexp(1.0, -s);
+          ym = small_solve<CPLX>(nb, b00, b10, b01, b11, wr, wi, smin, r0r * f, r0i * f, r1r * f, r1i * f, y0r, y0i,
+                                 y1r, y1i);
+          if (ym <= kOmega || s > 4000) break;
+          ++s;
+        }
+        const double f = ldexp(1.0, -s);
 #pragma unroll
-      for (int j = 0; j < kRegs; ++j) { vr[j] *= f; vi[j] *= f; }
-      scale_rows(a.Y, a.ldY, U.col, ncol, 0, a.i0, f, lane);
-      scale_rows(a.Y, a.ldY, U.col, ncol, below0, below1, f, lane);
-      stt.bound *= f;
-      ynorm *= f;
-      B *= f;
-      e += s;
-      if (lane == 0) atomicAdd(a.rescales, 1);
-    }
-    // the solved rows replace their right-hand side
-    if (lane == l0) { reg_set(vr, j0, y0r); reg_set(vi, j0, y0i); }
-    if (nb == 2 && lane == l1) { reg_set(vr, j1, y1r); reg_set(vi, j1, y1i); }
-    ynorm = fmax(ynorm, ym);
-    if (i == 0) break;
-    // update of the tile rows above: protect with the running bound
-    double cm = cmx[i];
-    if (nb == 2) cm = fmax(cm, cmx[i + 1]);
-    const double g = B / kOmega + ((double)nb * (ym / kOmega)) * cm;
-    if (g > 1.0) {
-      const int s = rescale_steps(g, fmax(fmax(B, ym), ynorm));
-      const double f = ldexp(1.0, -s);
+        for (int j = 0; j < kRegs; ++j) { vr[j] *= f; vi[j] *= f; }
+        scale_rows(a.Y, a.ldY, U.col, ncol, 0, a.i0, f, lane);
+        scale_rows(a.Y, a.ldY, U.col, ncol, below0, below1, f, lane);
+        stt.bound *= f;
+        ynorm *= f;
+        B *= f;
+        e += s;
+        if (lane == 0) atomicAdd(a.rescales, 1);
+      }
+      // the solved rows replace their right-hand side
+      if (lane == l0) { vr[J] = y0r; if (CPLX) vi[J] = y0i; }
+      if (nb == 2) {
+        if (up) {
+          if (J + 1 < kRegs && lane == 0) {
+            vr[J + 1 < kRegs ? J + 1 : J] = y1r;
+            if (CPLX) vi[J + 1 < kRegs ? J + 1 : J] = y1i;
+          }
+        } else if (lane == l0 + 1) {
+          vr[J] = y1r;
+          if (CPLX) vi[J] = y1i;
+        }
+      }
+      ynorm = fmax(ynorm, ym);
+      if (i == 0) break;
+      // update of the tile rows above: protect with the running bound
+      double cm = cmx[i];
+      if (nb == 2) cm = fmax(cm, cmx[i + 1]);
+      const double g = B / kOmega + ((double)nb * (ym / kOmega)) * cm;
+      if (g > 1.0) {
+        const int s = rescale_steps(g, fmax(fmax(B, ym), ynorm));
+        const double f = ldexp(1.0, -s);
 #pragma unroll
-      for (int j = 0; j < kRegs; ++j) { vr[j] *= f; vi[j] *= f; }
-      y0r *= f; y0i *= f; y1r *= f; y1i *= f;
-      scale_rows(a.Y, a.ldY, U.col, ncol, 0, a.i0, f, lane);
-      scale_rows(a.Y, a.ldY, U.col, ncol, below0, below1, f, lane);
-      stt.bound *= f;
-      ynorm *= f;
-      B *= f;
-      ym *= f;
-      e += s;
-      if (lane == 0) atomicAdd(a.rescales, 1);
-    }
-    B += (double)nb * cm * ym;
+        for (int j = 0; j < kRegs; ++j) { vr[j] *= f; vi[j] *= f; }
+        y0r *= f; y0i *= f; y1r *= f; y1i *= f;
+        scale_rows(a.Y, a.ldY, U.col, ncol, 0, a.i0, f, lane);
+        scale_rows(a.Y, a.ldY, U.col, ncol, below0, below1, f, lane);
+        stt.bound *= f;
+        ynorm *= f;
+        B *= f;
+        ym *= f;
+        e += s;
+        if (lane == 0) atomicAdd(a.rescales, 1);
+      }
+      B += (double)nb * cm * ym;
+      // register J: the lanes above the block; registers below J: every lane
+      {
+        const int r = lane + 32 * J;
+        if (lane < l0) {
+          const double s0 = Ts[r + i * kLdT];
+          double xr = vr[J] - s0 * y0r, xi = CPLX ? vi[J] - s0 * y0i : 0.0;
+          if (nb == 2) {
+            const double s1 = Ts[r + (i + 1) * kLdT];
+            xr -= s1 * y1r;
+            if (CPLX) xi -= s1 * y1i;
+          }
+          vr[J] = xr;
+          if (CPLX) vi[J] = xi;
+        }
+      }
 #pragma unroll
-    for (int j = 0; j < kRegs; ++j) {
-      const int r = lane + 32 * j;
-      if (r < i) {
+      for (int j = 0; j < J; ++j) {
+        const int r = lane + 32 * j;
         const double s0 = Ts[r + i * kLdT];
-        double xr = vr[j] - s0 * y0r, xi = vi[j] - s0 * y0i;
+        double xr = vr[j] - s0 * y0r, xi = CPLX ? vi[j] - s0 * y0i : 0.0;
         if (nb == 2) {
           const double s1 = Ts[r + (i + 1) * kLdT];
           xr -= s1 * y1r;
-          xi -= s1 * y1i;
+          if (CPLX) xi -= s1 * y1i;
         }
         vr[j] = xr;
-        vi[j] = xi;
+        if (CPLX) vi[j] = xi;
       }
     }
   }
