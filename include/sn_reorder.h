@@ -67,7 +67,13 @@ typedef struct sn_opts {
                                 stream and report per-kernel-kind times in sn_stats */
   int32_t lookahead;         /* 1 (default): the next level's window kernel waits only for the
                                 update strips it reads; the rest overlaps it on a third stream */
-  int32_t reserved;
+  int32_t fuse_chain;        /* row f1: 1 = fuse the Q updates of two
+                                consecutive windows x, y of a chain (y at the next level, above x,
+                                overlapping it; no other window of y's level touching x's
+                                columns): x's Q update is deferred to y's level and one CTA pass
+                                per Q strip applies Zx, then Zy.  Results are bitwise those of the
+                                unfused run.  Needs TMA-describable Q (16-byte aligned, even
+                                ldQ), else ignored.  Default 0 (measured slower). */
 } sn_opts;
 
 /* Statistics of one call. */
@@ -97,6 +103,7 @@ typedef struct sn_stats {
   double g3_max_ratio;       /* generalized path: the largest stability-test residual ratio
                                 (residual / threshold, G3) among the accepted swaps -- the
                                 decision margin; 0 elsewhere */
+  int64_t fused_q_pairs;     /* opts.fuse_chain: window pairs whose Q updates ran fused */
 } sn_stats;
 
 void sn_default_opts(sn_opts* o);

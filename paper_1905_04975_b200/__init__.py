@@ -50,7 +50,7 @@ class Opts(C.Structure):
     _fields_ = [("window", C.c_int64), ("inner_window", C.c_int64), ("max_windows", C.c_int64),
                 ("force_reject_window", C.c_int64), ("force_reject_swap", C.c_int64),
                 ("validate_lower", C.c_int32), ("serialize", C.c_int32), ("q_stream_overlap", C.c_int32),
-                ("profile", C.c_int32), ("lookahead", C.c_int32), ("reserved", C.c_int32)]
+                ("profile", C.c_int32), ("lookahead", C.c_int32), ("fuse_chain", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -62,7 +62,7 @@ class Stats(C.Structure):
                 ("ms_total", C.c_double), ("ms_h2d", C.c_double), ("ms_d2h", C.c_double),
                 ("launches", C.c_int64 * 5), ("ms_kernel", C.c_double * 5), ("flops_kernel", C.c_double * 5),
                 ("bytes_kernel", C.c_double * 5), ("flops_exec_kernel", C.c_double * 5),
-                ("g3_max_ratio", C.c_double)]
+                ("g3_max_ratio", C.c_double), ("fused_q_pairs", C.c_int64)]
 
     def to_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}

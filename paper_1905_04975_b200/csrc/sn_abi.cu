@@ -358,6 +358,35 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
     lookahead_strips(P, NT, cl, cr);          // schedule order -> level-sorted order
     for (int64_t i = 0; i < nw; ++i) { critL[i] = cl[sorted[i]]; critR[i] = cr[sorted[i]]; }
   }
+  // Row f1, fused chain updates (opts.fuse_chain): the Q update of a window x moves to the
+  // level of its chain successor y (next in schedule order, one level later, above x and
+  // overlapping it), whose Q launch applies Zx then Zy to each Q strip in one CTA pass.  No
+  // other window of y's level may touch x's columns; pairs are disjoint (a y is never an x).
+  std::vector<int32_t> qprev(nw, 0);    // level-sorted: 1 + level-sorted index of the predecessor
+  std::vector<uint8_t> qdefer(nw, 0);   // level-sorted: Q update applied by the successor's launch
+  const bool fuseQ = o.fuse_chain != 0 && Q != nullptr && ((uintptr_t)Q % 16) == 0 && (ldQ % 2) == 0;
+  int64_t fused_pairs = 0;
+  if (fuseQ) {
+    std::vector<int64_t> pos_of(nw);
+    for (int64_t i = 0; i < nw; ++i) pos_of[sorted[i]] = i;
+    std::vector<uint8_t> isy(nw, 0);   // schedule order
+    for (int64_t t = 0; t + 1 < nw; ++t) {
+      if (isy[t]) continue;
+      const WindowPlan& x = P.wins[t];
+      const WindowPlan& y = P.wins[t + 1];
+      if (y.level != x.level + 1 || y.j1 >= x.j1 || y.j1 + y.k <= x.j1) continue;
+      bool ok = true;
+      for (int64_t i = lstart[y.level]; i < lstart[y.level + 1] && ok; ++i) {
+        const WindowPlan& w = P.wins[sorted[i]];
+        if (sorted[i] != t + 1 && w.j1 < x.j1 + x.k && w.j1 + w.k > x.j1) ok = false;
+      }
+      if (!ok) continue;
+      isy[t + 1] = 1;
+      qprev[pos_of[t + 1]] = (int32_t)(pos_of[t] + 1);
+      qdefer[pos_of[t]] = 1;
+      ++fused_pairs;
+    }
+  }
   for (int64_t l = 0; l < P.nlevels; ++l) {
     const int64_t a = lstart[l], b = lstart[l + 1];
     for (int kind = 0; kind < NK; ++kind) {
@@ -373,7 +402,7 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
           case 1: cnt = look ? nL - critL[i] : 0; break;
           case 2: cnt = look ? critR[i] : nR; break;
           case 3: cnt = look ? nR - critR[i] : 0; break;
-          default: cnt = Q ? (n + NT - 1) / NT : 0; break;
+          default: cnt = (Q && !qdefer[i]) ? (n + NT - 1) / NT : 0; break;
         }
         acc += (int32_t)cnt;
         pref.push_back(acc);
@@ -387,7 +416,7 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
       d.slot = (int32_t)((l % kZgen) * maxper + (i - a));
       d.pool = w.pool; d.order = w.order;
       d.crit_l = critL[i]; d.crit_r = critR[i];
-      d.coff = 0; d.sidx = (int32_t)i; d.pad = 0;
+      d.coff = 0; d.sidx = (int32_t)i; d.qprev = qprev[i];
     }
   }
   const double t_plan = now_ms();
@@ -437,6 +466,7 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
   PanelMaps mapS{}, mapQ{};
   panel_maps_init(&mapS, dZ, (int64_t)kZgen * maxper, S, n, n, ldS);
   if (Q) panel_maps_init(&mapQ, dZ, (int64_t)kZgen * maxper, Q, n, n, ldQ);
+  if (fuseQ && !mapQ.valid) return SN_ERR_UNSUPPORTED;   // fused passes: TMA kernel only
   unsigned long long* dtp = nullptr;   // SN_WPROF: window-kernel phase cycles (debug)
   if (std::getenv("SN_WPROF")) {
     CK(cudaMalloc(&dtp, 16 * sizeof(unsigned long long)));
@@ -469,7 +499,10 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
     const int gen = (int)(l % kZgen);
     cur_level = l;
     nvtxRangePushA("sn level");
-    if (overlapQ && l >= kZgen) CK(cudaStreamWaitEvent(sA, ws.evQ[gen], 0));
+    // Z slots of generation gen are rewritten: the Q launch that last read them must be done
+    // (with fused Q updates that is the launch of the level after their own)
+    if (overlapQ && !fuseQ && l >= kZgen) CK(cudaStreamWaitEvent(sA, ws.evQ[gen], 0));
+    if (overlapQ && fuseQ && l >= kZgen) CK(cudaStreamWaitEvent(sA, ws.evQ[(l + 1) % kZgen], 0));
     WindowArgs wa{};
     wa.wins = dw + a; wa.nwin = (int32_t)cnt; wa.base = (int32_t)a;
     wa.pool = (const uint8_t*)ws.pool.p; wa.S = S; wa.ldS = ldS; wa.Z = dZ;
@@ -519,6 +552,7 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
       pa.vec16 = (ldQ % 2 == 0 && ((uintptr_t)Q % 16) == 0) ? 1 : 0;
       pa.prefix = dpref + pref_off[l * NK + 4];
       pa.part = 0;
+      pa.fuse = fuseQ ? 1 : 0;
       pe = prof_begin(3, sQ);
       launch_panel(2, mt, pa, nstrips[l * NK + 4], sQ);
       prof_end(pe, sQ);
@@ -654,6 +688,7 @@ int run_on(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* Q, int64
       st->bytes_kernel[q] = bk[q];
       st->flops_exec_kernel[q] = fx[q];
     }
+    st->fused_q_pairs = fused_pairs;
   }
   return ctl.abort ? SN_ERR_REJECTED : SN_OK;
 }

@@ -30,7 +30,9 @@ struct WinDev {
   int64_t coff;      // column offset: column j of S is stored at column j + coff of the
                      // array passed (0 on one GPU; the extended local layout when sharded)
   int32_t sidx;      // index of this window in the status array (level-sorted order)
-  int32_t pad;
+  int32_t qprev;     // fused chain Q update (PanelArgs.fuse): 1 + level-sorted index of the
+                     // chain predecessor whose Q update this window's Q launch applies first
+                     // (0: none)
 };
 
 // One panel segment given explicitly (the sharded executor, sn_dist.h): window index within
@@ -119,6 +121,9 @@ struct PanelArgs {
   const double* Z;
   const int16_t* zrange;    // per slot row intervals of Z's columns (window kernel output)
   const PanelMaps* maps;    // host pointer: TMA descriptors (NULL or !valid: cp.async kernel)
+  int32_t fuse;             // Q kind, TMA kernel only: apply WinDev.qprev's Z to a strip, then
+                            // this window's Z, in one pass of the CTA (row f1)
+  int32_t pad;
 };
 
 // per-device launch state (function attributes are set once per device)

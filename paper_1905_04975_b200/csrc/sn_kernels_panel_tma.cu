@@ -4,6 +4,10 @@
 //   left  (kind 0):  S[j1:j2, strip]  <- Z^T * S[j1:j2, strip]
 //   right (kind 1):  S[strip, j1:j2]  <- S[strip, j1:j2] * Z
 //   Q     (kind 2):  Q[strip, j1:j2]  <- Q[strip, j1:j2] * Z
+//   Q fused (kind 3, row f1): Q[strip, x1:x2] <- Q[strip, x1:x2] * Zx, then
+//                     Q[strip, y1:y2] <- Q[strip, y1:y2] * Zy for two consecutive windows x, y of
+//                     a chain, in one CTA pass per strip (the second pass's TMA loads wait on an
+//                     mbarrier the consumer warps release after storing the first pass)
 // CTA = MT/32 consumer warps (each a 32 x 64 tile of the MT x 64 strip result, MI = 2 m16
 // tiles x NI = 8 n8 tiles of mma.sync.m16n8k4 f64 = DMMA) + 1 producer warp whose elected
 // lane streams K chunks (16 rows of Z^T and of the strip) with cp.async.bulk.tensor (TMA)
@@ -48,7 +52,7 @@ struct TCfg {
   static constexpr int A_BYTES = 8 * LDA * MT;
   static constexpr int B_BYTES = 8 * (LDBR * KC > LDBL * NT ? LDBR * KC : LDBL * NT);
   static constexpr int STAGE = ((A_BYTES + B_BYTES + 1023) / 1024) * 1024;
-  static constexpr size_t SMEM = (size_t)STAGE * NS + 1024 + 2 * 8 * NS;
+  static constexpr size_t SMEM = (size_t)STAGE * NS + 1024 + 2 * 8 * NS + 8;
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -99,6 +103,10 @@ struct StripInfo {
   int64_t x0, j1, jc;
   int slot;
   bool skip;
+  // fused chain Q update (a.fuse): the predecessor's pass, applied first when pdo
+  bool pdo;
+  int pk, pnk, pslot;
+  int64_t pjc;
 };
 
 template <int KIND>
@@ -144,6 +152,17 @@ __device__ __forceinline__ StripInfo resolve(const PanelArgs& a, int sid) {
   s.j1 = wd.j1;
   s.jc = (KIND == 1) ? wd.j1 + wd.coff : wd.j1;
   s.slot = wd.slot;
+  s.pdo = false;
+  s.pk = 0; s.pnk = 0; s.pslot = 0; s.pjc = 0;
+  if (KIND == 3 && wd.qprev > 0) {
+    const int pidx = wd.qprev - 1;                 // level-sorted index (a.wins == base + a.base)
+    const WinDev& pd = a.wins[pidx - a.base];
+    s.pdo = a.status[pidx] != kWinSkipped;
+    s.pk = pd.k;
+    s.pnk = (pd.k + KC - 1) / KC;
+    s.pslot = pd.slot;
+    s.pjc = pd.j1 + pd.coff;
+  }
   return s;
 }
 
@@ -159,12 +178,14 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
   unsigned char* smem = smem_raw + ((1024u - (sa(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = (uint64_t*)(smem + (size_t)C::STAGE * C::NS);
   uint64_t* empty = full + C::NS;
+  uint64_t* wb = empty + C::NS;     // fused Q passes: first pass stored (one arrival per consumer warp)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < C::NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::CONS);
     }
+    mbar_init(wb, C::CONS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -176,11 +197,21 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
   if (warp == C::CONS) {
     // ---------------- producer: one elected lane issues every TMA
     // the whole warp walks the schedule (warp-uniform values); one elected lane issues
-    uint32_t it = 0;
+    uint32_t it = 0, wbuse = 0;
     for (int sid = s_begin; sid < nstrips; sid += s_step) {
       const StripInfo si = resolve<KIND>(a, sid);
-      if (si.skip) continue;
-      for (int kc = 0; kc < si.nk; ++kc, ++it) {
+      // passes: the fused predecessor's Z (p = 0), then this window's (p = 1)
+      for (int p = si.pdo ? 0 : 1; p < 2; ++p) {
+      if (p == 1 && si.skip) break;
+      if (p == 1 && si.pdo) {
+        // the second pass reads columns the first pass wrote: wait until every consumer warp
+        // has stored them and fenced them for the async proxy
+        mbar_wait(wb, wbuse & 1);
+        ++wbuse;
+      }
+      const int pnk = p ? si.nk : si.pnk, pslot = p ? si.slot : si.pslot;
+      const int64_t pjc = p ? si.jc : si.pjc;
+      for (int kc = 0; kc < pnk; ++kc, ++it) {
         const int st = it % C::NS;
         mbar_wait(&empty[st], ((it / C::NS) & 1) ^ 1);
         unsigned char* As = smem + (size_t)st * C::STAGE;
@@ -192,16 +223,17 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
             const uint32_t txA = 8u * LDA * MT, txB = kTx - txA;
             mbar_expect_tx(&full[st], (dbg & 4) ? txA : (dbg & 8) ? txB : kTx);
             // A: As[m][0..19] = Z[kc*16 + 0..19, m] of the window's slot (Z columns m < MT)
-            if (!(dbg & 8)) tma_2d(As, &zmap, kc * KC, si.slot * kZld, &full[st]);
+            if (!(dbg & 8)) tma_2d(As, &zmap, kc * KC, pslot * kZld, &full[st]);
             if (!(dbg & 4)) {
               // the inner box coordinate must be 16-byte aligned: start one row early for odd
               // j1 (the consumers read with the offset j1 & 1; the box has 4 rows of slack)
               if (LEFT) tma_2d(Bs, &mmap, (int)((si.j1 + kc * KC) & ~(int64_t)1), (int)si.x0, &full[st]);  // Bs[c][kk]
-              else tma_2d(Bs, &mmap, (int)si.x0, (int)(si.jc + kc * KC), &full[st]);         // Bs[kk][r]
+              else tma_2d(Bs, &mmap, (int)si.x0, (int)(pjc + kc * KC), &full[st]);           // Bs[kk][r]
             }
           }
         }
         __syncwarp();
+      }
       }
     }
     __syncwarp();
@@ -214,11 +246,14 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
   uint32_t it = 0;
   for (int sid = s_begin; sid < nstrips; sid += s_step) {
     const StripInfo si = resolve<KIND>(a, sid);
-    if (si.skip) continue;
+    for (int p = si.pdo ? 0 : 1; p < 2; ++p) {
+    if (p == 1 && si.skip) break;
+    const int pk = p ? si.k : si.pk, pnk = p ? si.nk : si.pnk, pslot = p ? si.slot : si.pslot;
+    const int64_t pjc = p ? si.jc : si.pjc;
     // K interval of this warp's 32 output rows (Z structure; exact zeros outside)
     int wlo, whi;
     {
-      const int16_t* zr = a.zrange + (int64_t)si.slot * kZrange;
+      const int16_t* zr = a.zrange + (int64_t)pslot * kZrange;
       int lo = zr[wm0 + lane], hi = zr[kZld + wm0 + lane];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -236,7 +271,7 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
       for (int j = 0; j < 8; ++j)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
-    for (int kc = 0; kc < si.nk; ++kc, ++it) {
+    for (int kc = 0; kc < pnk; ++kc, ++it) {
       const int st = it % C::NS;
       mbar_wait(&full[st], (it / C::NS) & 1);
       const double* As = (const double*)(smem + (size_t)st * C::STAGE);
@@ -276,16 +311,24 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int m = wm0 + i * 16 + g + 8 * h;
-          if (m >= si.k) continue;
+          if (m >= pk) continue;
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int xx = j * 8 + 2 * t + q;
             if (xx >= si.nx) continue;
             const double v = acc[i][j][2 * h + q];
             if (LEFT) M[(si.j1 + m) + (si.x0 + xx) * ld] = v;
-            else M[(si.x0 + xx) + (si.jc + m) * ld] = v;
+            else M[(si.x0 + xx) + (pjc + m) * ld] = v;
           }
         }
+    if (p == 0 && !si.skip) {
+      // the second pass's TMA loads read these columns: order the generic stores before the
+      // async proxy, then release them to the producer
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(wb);
+    }
+    }
   }
 }
 
@@ -379,14 +422,17 @@ void launch_panel_tma(int kind, int mt, const PanelArgs& a, int32_t nstrips, con
   if (mt <= 64) {
     if (kind == 0) launch_tma_t<64, 0>(a, nstrips, pm, st);
     else if (kind == 1) launch_tma_t<64, 1>(a, nstrips, pm, st);
+    else if (a.fuse) launch_tma_t<64, 3>(a, nstrips, pm, st);
     else launch_tma_t<64, 2>(a, nstrips, pm, st);
   } else if (mt <= 128) {
     if (kind == 0) launch_tma_t<128, 0>(a, nstrips, pm, st);
     else if (kind == 1) launch_tma_t<128, 1>(a, nstrips, pm, st);
+    else if (a.fuse) launch_tma_t<128, 3>(a, nstrips, pm, st);
     else launch_tma_t<128, 2>(a, nstrips, pm, st);
   } else {
     if (kind == 0) launch_tma_t<256, 0>(a, nstrips, pm, st);
     else if (kind == 1) launch_tma_t<256, 1>(a, nstrips, pm, st);
+    else if (a.fuse) launch_tma_t<256, 3>(a, nstrips, pm, st);
     else launch_tma_t<256, 2>(a, nstrips, pm, st);
   }
 }

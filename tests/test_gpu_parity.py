@@ -364,3 +364,54 @@ def test_natural_rejection_matches_oracle():
         nS = np.linalg.norm(S)
         assert np.abs(St.cpu().numpy().T - ref["S"]).max() <= TOL * nS
         assert np.abs(Qt.cpu().numpy().T - ref["Q"]).max() <= TOL * nS
+
+
+@pytest.mark.parametrize("n,w,opts", [(2500, 256, {}), (1500, 64, {}), (1300, 128, {}),
+                                      (2200, 256, dict(q_stream_overlap=0)),
+                                      (2200, 256, dict(lookahead=0, serialize=1))])
+def test_fused_chain_q_bitwise(n, w, opts):
+    """Row f1, fused chain updates (opts.fuse_chain): the Q updates of consecutive
+    windows of a chain applied in one CTA pass per Q strip give bitwise the unfused result
+    (each pass is the same arithmetic sequence; the fusion changes only when and where)."""
+    p = make_problem(n, p2=0.25, q="householder", psel=0.35, w=w, seed=40 + n % 7)
+    outs = []
+    for fuse in (0, 1):
+        S, Q = p.S.cuda(), p.Q.cuda()
+        r = sn.reorder(S, Q, p.select, window=w, fuse_chain=fuse, **opts)
+        torch.cuda.synchronize()
+        outs.append((r, S.cpu(), Q.cpu()))
+    (r0, S0, Q0), (r1, S1, Q1) = outs
+    assert r0["rc"] == r1["rc"] == 0
+    assert r0["stats"]["fused_q_pairs"] == 0 and r1["stats"]["fused_q_pairs"] > 0
+    print("n=%d w=%d %s: %d fused pairs of %d windows" % (n, w, opts, r1["stats"]["fused_q_pairs"],
+                                                         r1["stats"]["windows"]))
+    assert torch.equal(S0, S1) and torch.equal(Q0, Q1)
+    np.testing.assert_array_equal(r0["bmap"], r1["bmap"])
+
+
+def test_fused_chain_q_oracle_parity():
+    """The fused executor against the oracle (the bar of the unfused path)."""
+    p = make_problem(1700, p2=0.25, q="householder", psel=0.35, w=256, seed=41)
+    S0, Q0, ref, got, Sg, Qg = run_both(p, fuse_chain=1)
+    assert got["stats"]["fused_q_pairs"] > 0
+    assert_parity(S0, Q0, ref, got, Sg, Qg, "fuse_chain")
+
+
+def test_fused_chain_q_forced_rejection():
+    """A rejection inside a fused pair's levels: the predecessor's Q pass still runs when its
+    successor is skipped, so the state equals the unfused run's bitwise."""
+    p = make_problem(1400, p2=0.25, q="householder", psel=0.4, w=64, seed=22)
+    sch = sn.reorder(p.S.cuda(), p.Q.cuda(), p.select, window=64, fuse_chain=1)
+    assert sch["stats"]["fused_q_pairs"] > 0
+    outs = []
+    for t in (sch["stats"]["windows"] // 3, sch["stats"]["windows"] // 2):
+        for fuse in (0, 1):
+            S, Q = p.S.cuda(), p.Q.cuda()
+            r = sn.reorder(S, Q, p.select, window=64, fuse_chain=fuse, force_reject_window=t,
+                           force_reject_swap=1)
+            torch.cuda.synchronize()
+            assert r["rc"] == sn.SN_ERR_REJECTED
+            outs.append((r, S.cpu(), Q.cpu()))
+        (ra, Sa, Qa), (rb, Sb, Qb) = outs[-2:]
+        assert torch.equal(Sa, Sb) and torch.equal(Qa, Qb)
+        np.testing.assert_array_equal(ra["bmap"], rb["bmap"])
