@@ -304,6 +304,24 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
     // every K chunk of this strip has landed and been consumed: overwrite in place
     double* M = a.M;
     const int64_t ld = a.ld;
+    if (!LEFT && (si.x0 & 1) == 0 && !(dbg & 16)) {   // SN_TMA_DBG bit 16: scalar stores (A/B)
+      // right / Q: a lane's two accumulators of one row pair are adjacent strip rows (column-
+      // major), 16-byte aligned (TMA-described M: aligned base, even ld; even x0): one 16-byte
+      // store, four lanes filling 64 contiguous bytes of a column
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int m = wm0 + i * 16 + g + 8 * h;
+            const int xx = j * 8 + 2 * t;
+            if (m >= pk || xx >= si.nx) continue;
+            double* dst = M + (si.x0 + xx) + (pjc + m) * ld;
+            if (xx + 1 < si.nx) *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][2 * h], acc[i][j][2 * h + 1]);
+            else dst[0] = acc[i][j][2 * h];
+          }
+    } else {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -321,6 +339,7 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
             else M[(si.x0 + xx) + (pjc + m) * ld] = v;
           }
         }
+    }
     if (p == 0 && !si.skip) {
       // the second pass's TMA loads read these columns: order the generic stores before the
       // async proxy, then release them to the producer
