@@ -74,6 +74,11 @@ typedef struct sn_opts {
                                 per Q strip applies Zx, then Zy.  Results are bitwise those of the
                                 unfused run.  Needs TMA-describable Q (16-byte aligned, even
                                 ldQ), else ignored.  Default 0 (measured slower). */
+  int32_t pencil_cluster;    /* row f2 (sn_reorder_pencil_ex): CTAs per window task, run as one
+                                thread-block cluster that splits the window's row / column
+                                applications (every CTA evaluates the step's transforms, so the
+                                results are bitwise those of one CTA).  0 (default) = auto (as many
+                                as the level's windows leave SMs for, <= 8), 1 = one CTA, 2..8. */
 } sn_opts;
 
 /* Statistics of one call. */

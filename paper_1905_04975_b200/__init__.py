@@ -19,6 +19,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libsn_b200.so")
+# A/B timing tools only: load another prebuilt in-tree copy of the library (never rebuilt)
+_LIB_OVERRIDE = os.environ.get("SN_LIB_PATH")
+if _LIB_OVERRIDE:
+    LIB_PATH = os.path.abspath(_LIB_OVERRIDE)
 CSRC = os.path.join(_HERE, "csrc")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
@@ -30,6 +34,8 @@ def sources():
 
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile the CUDA library for sm_100a (nvcc; works without a GPU)."""
+    if _LIB_OVERRIDE:
+        return LIB_PATH
     srcs = sources()
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     deps.append(os.path.join(_ROOT, "include", "sn_reorder.h"))
@@ -50,7 +56,8 @@ class Opts(C.Structure):
     _fields_ = [("window", C.c_int64), ("inner_window", C.c_int64), ("max_windows", C.c_int64),
                 ("force_reject_window", C.c_int64), ("force_reject_swap", C.c_int64),
                 ("validate_lower", C.c_int32), ("serialize", C.c_int32), ("q_stream_overlap", C.c_int32),
-                ("profile", C.c_int32), ("lookahead", C.c_int32), ("fuse_chain", C.c_int32)]
+                ("profile", C.c_int32), ("lookahead", C.c_int32), ("fuse_chain", C.c_int32),
+                ("pencil_cluster", C.c_int32)]
 
 
 class Stats(C.Structure):

@@ -490,8 +490,8 @@ __device__ __forceinline__ bool pl_transform(const double* Sw, int64_t ldS, cons
   for (int c = 0; c < m; ++c)
 #pragma unroll
     for (int r = 0; r < m; ++r) {
-      A[r + 4 * c] = Sw[(j + r) + (int64_t)(j + c) * ldS];
-      B[r + 4 * c] = Tw[(j + r) + (int64_t)(j + c) * ldT];
+      A[r + 4 * c] = __ldcg(Sw + (j + r) + (int64_t)(j + c) * ldS);
+      B[r + 4 * c] = __ldcg(Tw + (j + r) + (int64_t)(j + c) * ldT);
     }
   double U[16], V[16], An[16], Bn[16];
   const bool ok = pl_swap_t<N1, N2>(A, B, U, V, An, Bn, why);
@@ -532,6 +532,7 @@ struct PencilWinArgs {
   Control* ctl;
   int64_t force_order;
   int32_t force_swap;
+  unsigned long long* pprof;   // debug (SN_PPROF): cycles per phase summed over windows, or NULL
 };
 
 // index i with pre[i] <= q < pre[i + 1]
@@ -544,10 +545,36 @@ __device__ __forceinline__ int pl_find(const int* pre, int cnt, int q) {
   return lo;
 }
 
+__device__ __forceinline__ unsigned pl_cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned pl_cluster_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+
+// Window task on a thread-block cluster of C CTAs (C = 1: a plain CTA).  Every CTA evaluates
+// all transforms of a step (identical arithmetic, so identical records and rejection
+// decisions) and the block-size bookkeeping in its own shared memory; the row and column
+// applications -- the bulk of the work -- are split over the C x 256 threads.  Phases that
+// read what another CTA wrote are separated by cluster barriers (release / acquire), and every
+// global read of the window, T, UL and VR bypasses L1 (ld.global.cg), so no CTA sees a stale
+// line of another SM's writes.
 __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   extern __shared__ double rec[];            // kRecD doubles per swap of the current step
-  const WinDev wd = a.wins[blockIdx.x];
+  const unsigned C = pl_cluster_size(), rank = pl_cluster_rank();
+  const WinDev wd = a.wins[blockIdx.x / C];
   const int tid = threadIdx.x;
+  const int gt = (int)rank * (int)blockDim.x + tid, GC = (int)(C * blockDim.x);   // cluster thread id / count
+  auto csync = [&]() {
+    if (C > 1)
+      asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else
+      __syncthreads();
+  };
   const int k = wd.k;
   double* Sw = a.S + wd.j1 + wd.j1 * a.ldS;
   double* Tw = a.T + wd.j1 + wd.j1 * a.ldT;
@@ -561,7 +588,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   __shared__ int16_t s_lo[kZld], s_hi[kZld];   // merged nonzero row interval of its UL/VR columns
   __shared__ int s_rej;
   __shared__ double s_why[2];
-  for (int64_t i = tid; i < kZslot; i += blockDim.x) {
+  for (int64_t i = gt; i < kZslot; i += GC) {
     const int r = (int)(i % kZld), c = (int)(i / kZld);
     const double v = (r == c && c < k) ? 1.0 : 0.0;
     UL[i] = v;
@@ -572,11 +599,16 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     zhi[tid] = (int16_t)(tid < k ? tid : 0);
   }
   if (tid == 0) s_rej = 0x7fffffff;
-  __syncthreads();
+  csync();
   const int64_t s0 = a.swap_off[wd.sidx];
   const int32_t* soff = a.step_off + a.step_base[wd.sidx];
   const int nsteps = (int)(a.step_base[wd.sidx + 1] - a.step_base[wd.sidx]) - 1;
   int done_steps = 0;
+  unsigned long long pc[4] = {0, 0, 0, 0};   // transforms, intervals, rows, columns (tid 0, SN_PPROF)
+  long long pk = a.pprof && tid == 0 ? clock64() : 0;
+  auto ptick = [&](int q) {
+    if (a.pprof && tid == 0) { const long long c = clock64(); pc[q] += (unsigned long long)(c - pk); pk = c; }
+  };
   for (int st = 0; st < nsteps; ++st) {
     const int b0 = soff[st], cnt = soff[st + 1] - b0;
     // (1) transforms, one thread per swap
@@ -593,13 +625,14 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       else if (n2 == 1) ok = pl_transform<2, 1>(Sw, ldS, Tw, ldT, j, R, why);
       else ok = pl_transform<2, 2>(Sw, ldS, Tw, ldT, j, R, why);
       if (wd.order == a.force_order && a.sidx[s] == a.force_swap) { ok = false; why[0] = 0.0; }
-      if (ok) atomicMax(&a.ctl->ratio_bits, (unsigned long long)__double_as_longlong(why[1]));
+      if (ok && rank == 0) atomicMax(&a.ctl->ratio_bits, (unsigned long long)__double_as_longlong(why[1]));
       if (!ok) {
         const int key = a.sidx[s];
         if (atomicMin(&s_rej, key) > key) { s_why[0] = why[0]; s_why[1] = why[1]; }
       }
     }
-    __syncthreads();
+    csync();   // every CTA has read the diagonal blocks before any is overwritten
+    ptick(0);
     if (s_rej != 0x7fffffff) break;
     // (2) column intervals of the accumulators; row-application task counts
     if (tid < cnt) {
@@ -618,8 +651,9 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       }
     }
     __syncthreads();
+    ptick(1);
     // (3) rows j..j+m-1 right of each block (S, T); the new diagonal blocks
-    for (int q = tid; q < cnt * 16; q += blockDim.x) {
+    for (int q = gt; q < cnt * 16; q += GC) {
       const int i = q >> 4, d = q & 15, m = s_m[i];
       if (d >= m * m) continue;
       const int j = s_j[i], r = d % m, c = d / m;
@@ -662,13 +696,14 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     };
     for (int phase = 0; phase < 2; ++phase) {
       if (phase == 1) {
-        __syncthreads();
+        csync();   // row applications (all CTAs) before column applications (corner order)
+        ptick(2);
         if (tid == 0)
           for (int i = 0; i < cnt; ++i) s_pre[i + 1] = s_pre[i] + 2 * s_j[i] + 2 * (s_hi[i] - s_lo[i] + 1);
         __syncthreads();
       }
       const int total = s_pre[cnt];
-      for (int q0 = tid; q0 < total; q0 += 2 * blockDim.x) {
+      for (int q0 = gt; q0 < total; q0 += 2 * GC) {
         double* X[2];
         int64_t base[2], stride[2];
         const double* G[2];
@@ -676,14 +711,14 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
         double x[2][4];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const int q = q0 + u * blockDim.x;
+          const int q = q0 + u * GC;
           m[u] = 0;
           if (q < total) {
             if (phase == 0) row_task(q, X[u], base[u], stride[u], G[u], m[u]);
             else col_task(q, X[u], base[u], stride[u], G[u], m[u]);
           }
 #pragma unroll
-          for (int t = 0; t < 4; ++t) x[u][t] = t < m[u] ? X[u][base[u] + t * stride[u]] : 0.0;
+          for (int t = 0; t < 4; ++t) x[u][t] = t < m[u] ? __ldcg(X[u] + base[u] + t * stride[u]) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -702,10 +737,18 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       }
     }
     done_steps = st + 1;
-    __syncthreads();
+    csync();
+    ptick(3);
+  }
+  if (a.pprof && tid == 0 && rank == 0) {
+    for (int q = 0; q < 4; ++q) atomicAdd(&a.pprof[q], pc[q]);
+    atomicAdd(&a.pprof[4], (unsigned long long)nsteps);
+    atomicAdd(&a.pprof[5], 1ull);
+    atomicAdd(&a.pprof[6], (unsigned long long)(soff[nsteps] - soff[0]));
   }
   const int done = soff[done_steps] - soff[0];
   const int total = soff[nsteps] - soff[0];
+  if (rank != 0) return;
   if (tid < kZld) {
     int16_t* zr = a.zrange + (int64_t)wd.slot * kZrange;
     zr[tid] = zlo[tid];
@@ -753,6 +796,7 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
                cudaStream_t sA) {
   const double t0 = now_ms();
   int rc = 0;
+  DevBuf dpprof;
   DevBuf dsub, dbad, dwins, doff, dsj, ds12, dpref, dstatus, ddone, dctl, dUL, dVR, dzr, dstep, dstepb, didx;
   std::vector<uint8_t> sub((size_t)n);
   int32_t bad = 0;
@@ -912,11 +956,21 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
     panel_maps_init(&mTR, (double*)dVR.p, maxper, T, n, n, ldT);
     if (Q) panel_maps_init(&mQ, (double*)dUL.p, maxper, Q, n, n, ldQ);
     if (Zm) panel_maps_init(&mZ, (double*)dVR.p, maxper, Zm, n, n, ldZ);
+    if (std::getenv("SN_PPROF")) {
+      PK(dpprof.alloc(8 * sizeof(unsigned long long)));
+      PK(cudaMemsetAsync(dpprof.p, 0, 8 * sizeof(unsigned long long), sA));
+    }
     PK(cudaEventCreate(&e0));
     PK(cudaEventCreate(&e1));
     PK(cudaEventRecord(e0, sA));
     const int mt = o.window <= 64 ? 64 : (o.window <= 128 ? 128 : 256);
     const size_t smem_rec = sizeof(double) * kRecD * (size_t)max_step_cnt;
+    int num_sms = 148;
+    {
+      int dev = 0;
+      PK(cudaGetDevice(&dev));
+      PK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
     if (max_step_cnt > 256) { rc = SN_ERR_UNSUPPORTED; goto done; }
     PK(cudaFuncSetAttribute(pencil_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rec));
     for (int64_t l = 0; l < P.nlevels; ++l) {
@@ -930,7 +984,26 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
       wa.UL = (double*)dUL.p; wa.VR = (double*)dVR.p; wa.zrange = (int16_t*)dzr.p;
       wa.status = (int32_t*)dstatus.p; wa.done = (int32_t*)ddone.p; wa.ctl = (Control*)dctl.p;
       wa.force_order = o.force_reject_window; wa.force_swap = (int32_t)o.force_reject_swap;
-      pencil_window_kernel<<<(unsigned)(b - a), 256, smem_rec, sA>>>(wa);
+      wa.pprof = (unsigned long long*)dpprof.p;
+      {
+        // CTAs per window: as many as the level's windows leave SMs for (a cluster of <= 8)
+        int C = o.pencil_cluster;
+        if (C <= 0) C = (int)std::min<int64_t>(8, std::max<int64_t>(1, num_sms / (b - a)));
+        C = std::min(C, 8);
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at[1];
+        cfg.gridDim = dim3((unsigned)((b - a) * C));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem_rec;
+        cfg.stream = sA;
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)C;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        PK(cudaLaunchKernelEx(&cfg, pencil_window_kernel, wa));
+      }
       PK(cudaGetLastError());
       st->launches[0]++;
       auto panel = [&](int kind, double* M, int64_t ld, const double* Zs, const PanelMaps* pm) {
@@ -971,6 +1044,16 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
     PK(cudaMemcpy(hstatus.data(), dstatus.p, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
     PK(cudaMemcpy(hdone.data(), ddone.p, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
     PK(cudaMemcpy(&hctl, dctl.p, sizeof(Control), cudaMemcpyDeviceToHost));
+    if (dpprof.p) {
+      unsigned long long h[8];
+      PK(cudaMemcpy(h, dpprof.p, sizeof(h), cudaMemcpyDeviceToHost));
+      const double w = h[5] ? (double)h[5] : 1.0;
+      std::fprintf(stderr,
+                   "{\"probe\": \"pencil_window_phases\", \"windows\": %llu, \"steps_per_window\": %.1f, "
+                   "\"swaps_per_window\": %.1f, \"cycles_per_window\": {\"transform\": %.0f, \"intervals\": %.0f, "
+                   "\"rows\": %.0f, \"cols\": %.0f}}\n",
+                   h[5], h[4] / w, h[6] / w, h[0] / w, h[1] / w, h[2] / w, h[3] / w);
+    }
   }
   {
     // final block list: replay the executed swaps on the initial list (block at each first row)

@@ -206,3 +206,30 @@ def test_pencil_config2_size_completes_with_prefix_parity():
     np.testing.assert_array_equal(r["bmap"], exp_bmap)
     np.testing.assert_array_equal(check_gstructure(_host(dS), _host(dT)), exp_bmap)
     _gpu_invariants(S, T, Q, Z, dS, dT, dQ, dZ, 100 * n * np.finfo(float).eps)
+
+
+@pytest.mark.parametrize("n,p2,w,psel,seed,clusters", [
+    (513, 0.5, 128, 0.5, 6, (2, 3, 8)), (700, 0.25, 256, 0.2, 7, (0, 4)), (2000, 0.25, 128, 0.35, 12, (0,))])
+def test_pencil_cluster_split_bitwise(n, p2, w, psel, seed, clusters):
+    """opts.pencil_cluster: the window task on a cluster of C CTAs (every CTA evaluates the
+    step's transforms, the applications are split) gives bitwise the one-CTA result."""
+    p = make_pencil(n, p2=p2, q="householder", psel=psel, w=w, seed=seed)
+    _, r1 = _run(p, w, pencil_cluster=1)
+    assert r1["rc"] == 0
+    for c in clusters:
+        _, rc = _run(p, w, pencil_cluster=c)
+        assert rc["rc"] == 0
+        for key in ("S", "T", "Q", "Z"):
+            np.testing.assert_array_equal(rc[key], r1[key], err_msg="%s C=%d" % (key, c))
+        np.testing.assert_array_equal(rc["bmap"], r1["bmap"])
+        assert rc["stats"]["swaps"] == r1["stats"]["swaps"]
+
+
+def test_pencil_cluster_forced_rejection_bitwise():
+    p = make_pencil(400, p2=0.25, q="householder", psel=0.4, w=64, seed=11)
+    _, r1 = _run(p, 64, force_reject_window=3, force_reject_swap=40, pencil_cluster=1)
+    _, r4 = _run(p, 64, force_reject_window=3, force_reject_swap=40, pencil_cluster=4)
+    assert r1["rc"] == 1 == r4["rc"]
+    assert r1["stats"]["rejected_window"] == r4["stats"]["rejected_window"] == 3
+    for key in ("S", "T", "Q", "Z"):
+        np.testing.assert_array_equal(r4[key], r1[key])

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--cluster", type=int, default=0, help="opts.pencil_cluster (0 auto, 1 one CTA)")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     p = make_pencil(c["n"], c["p2"], c["q"], c["sel"], c["psel"], c["w"], seed=1, device="cuda")
@@ -32,7 +33,7 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        r = sn.reorder_pencil(S, T, Q, Z, p.select, window=c["w"])
+        r = sn.reorder_pencil(S, T, Q, Z, p.select, window=c["w"], pencil_cluster=args.cluster)
         e1.record(stream)
         torch.cuda.synchronize()
         if r["rc"] != 0:
@@ -49,7 +50,8 @@ def main():
         "probe": "pencil_reorder", "config": "config%d pencil (make_pencil): n=%d, w=%d" % (args.config, c["n"], c["w"]),
         "ms": ms, "eq_tflop": st["eq_flops"] / 1e12, "tflops_equivalent": st["eq_flops"] / (ms * 1e9),
         "windows": st["windows"], "levels": st["levels"], "swaps": st["swaps"],
-        "ms_device": st["ms_device"], "launches": st["launches"]}))
+        "ms_device": st["ms_device"], "launches": st["launches"], "pencil_cluster": args.cluster,
+        "times_ms": times}))
 
 
 if __name__ == "__main__":
