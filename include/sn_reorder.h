@@ -213,14 +213,16 @@ void sn_release_workspace(void);
  * triangular (not checked) with a diagonal 2x2 block on every 2x2 block of S.  The swap
  * transform follows the readings G1-G6 of DESIGN.md §3.1; on output every 2x2 block of T is
  * diagonal with t11 >= t22 > 0 and every 1x1 block of T that took part in a swap is >= 0.
- * S, T, Q, Z: DEVICE pointers (column-major fp64; Q and/or Z may be NULL), ld >= max(1, n);
- * the call is ordered on `stream` (a cudaStream_t, NULL = legacy default stream) and returns
- * when it has completed.  select/m/bmap_out/stats as sn_reorder_schur_ex (stats.eq_flops per
+ * S, T, Q, Z: column-major fp64 (Q and/or Z may be NULL), ld >= max(1, n), each a device or
+ * a host pointer: a host matrix is copied to a compact device copy before the reordering and
+ * back after it (also after SN_ERR_REJECTED), the caller keeping ownership; stats.ms_h2d /
+ * ms_d2h time those copies.  The call is ordered on `stream` (a cudaStream_t, NULL = legacy
+ * default stream) and returns when it has completed.  select/m/bmap_out/stats as sn_reorder_schur_ex (stats.eq_flops per
  * window 2k^2 (2(n-j2) + 2 j1 + n_Q + n_Z)).  opts: window, inner_window, max_windows,
  * force_reject_window/_swap and validate_lower are honoured.  Returns SN_OK,
  * SN_ERR_REJECTED (a swap failed the stability test: (S, T, Q, Z) hold a valid partially
  * reordered form that select / bmap_out describe), SN_ERR_CUDA, SN_ERR_UNSUPPORTED (options
- * out of range, or a host pointer), or -i for an invalid argument i (-2 also when S is not
+ * out of range), or -i for an invalid argument i (-2 also when S is not
  * quasi-triangular). */
 int sn_reorder_pencil_ex(const sn_opts* opts, int64_t n, double* S, int64_t ldS, double* T, int64_t ldT,
                          double* Q, int64_t ldQ, double* Z, int64_t ldZ, int32_t* select, int64_t* m,

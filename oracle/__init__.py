@@ -248,9 +248,11 @@ def gswap_last_variant() -> int:
 
 
 def greorder(S, T, Q, Z, select_rows, w: int, mode: int = 1, max_windows: int = -1,
-             force_reject_at: int = -1):
+             force_reject_at: int = -1, threads: int = 0):
     """Generalized reordering (Eq. (7) right form).  Returns dict(rc, S, T, Q, Z, select, m,
-    bmap, stats); all matrices Fortran fp64 copies."""
+    bmap, stats); all matrices Fortran fp64 copies.  threads > 0: the -fopenmp build of the
+    same code, its independent panel rows / columns on that many host threads (bitwise the
+    one-thread result, tests/test_oracle_generalized.py)."""
     Sx = _f64(S).copy(order="F"); Tx = _f64(T).copy(order="F")
     Qx = None if Q is None else _f64(Q).copy(order="F")
     Zx = None if Z is None else _f64(Z).copy(order="F")
@@ -260,7 +262,13 @@ def greorder(S, T, Q, Z, select_rows, w: int, mode: int = 1, max_windows: int = 
     bmap = np.zeros(n, np.int8)
     st = Stats()
     ld = max(n, 1)
-    rc = lib().or_greorder(mode, n, _ptr(Sx), ld, _ptr(Tx), ld, _ptr(Qx), ld, _ptr(Zx), ld, _ptr(sel),
+    L = lib()
+    if threads > 0:
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+        L = C.CDLL(build(omp=True))
+        L.or_greorder.argtypes = lib().or_greorder.argtypes
+        L.or_greorder.restype = C.c_int
+    rc = L.or_greorder(mode, n, _ptr(Sx), ld, _ptr(Tx), ld, _ptr(Qx), ld, _ptr(Zx), ld, _ptr(sel),
                            C.byref(m), w, max_windows, force_reject_at, _ptr(bmap), C.byref(st))
     stats = {f: getattr(st, f) for f, _ in Stats._fields_}
     stats["swaps_by_type"] = list(st.swaps_by_type)
@@ -321,7 +329,9 @@ def reorder_threads(S, Q, select_rows, w: int, threads: int, max_windows: int = 
     m = C.c_int64()
     bmap = np.zeros(n, np.int8)
     st = Stats()
-    rc = L.or_reorder_q(1, n, _ptr(Sx), max(n, 1), _ptr(Qx), max(n, 1), n, _ptr(sel), C.byref(m), w,
+    nq = n if Qx is None else Qx.shape[0]     # Q may hold a sample of rows, as in reorder()
+    assert Qx is None or Qx.shape[1] == n
+    rc = L.or_reorder_q(1, n, _ptr(Sx), max(n, 1), _ptr(Qx), max(nq, 1), nq, _ptr(sel), C.byref(m), w,
                         max_windows, -1, _ptr(bmap), C.byref(st))
     stats = {f: getattr(st, f) for f, _ in Stats._fields_}
     return {"rc": rc, "S": Sx, "Q": Qx, "select": sel, "m": m.value, "bmap": bmap, "stats": stats}

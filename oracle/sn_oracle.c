@@ -1253,30 +1253,63 @@ int or_gswap(int64_t nt, double* S, int64_t lds, double* T, int64_t ldt, int64_t
 }
 
 /* G6: the updates of one window of the generalized reordering (naive loops) */
+/* Every column (left) / row (right) is independent: with -fopenmp the loops run on several host
+ * threads, each keeping its own summation order, so the result does not depend on it (as
+ * window_updates_naive). */
 static void gpanel_left(int64_t n, double* A, int64_t lda, int64_t j1, int64_t j2, const double* U,
-                        double* tmp) {
+                        double* tmp0) {
   const int64_t k = j2 - j1;
-  for (int64_t c = j2; c < n; ++c) {
-    for (int64_t r = 0; r < k; ++r) {
-      double acc = 0.0;
-      for (int64_t l = 0; l < k; ++l) acc += U[l + r * k] * IDX(A, lda, j1 + l, c);
-      tmp[r] = acc;
+#ifdef _OPENMP
+#pragma omp parallel
+#endif
+  {
+#ifdef _OPENMP
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)k);
+#pragma omp for schedule(static)
+#else
+    double* tmp = tmp0;
+#endif
+    for (int64_t c = j2; c < n; ++c) {
+      for (int64_t r = 0; r < k; ++r) {
+        double acc = 0.0;
+        for (int64_t l = 0; l < k; ++l) acc += U[l + r * k] * IDX(A, lda, j1 + l, c);
+        tmp[r] = acc;
+      }
+      for (int64_t r = 0; r < k; ++r) IDX(A, lda, j1 + r, c) = tmp[r];
     }
-    for (int64_t r = 0; r < k; ++r) IDX(A, lda, j1 + r, c) = tmp[r];
+#ifdef _OPENMP
+    free(tmp);
+#endif
   }
+  (void)tmp0;
 }
 
 static void gpanel_right(int64_t rows, double* A, int64_t lda, int64_t j1, int64_t j2, const double* V,
-                         double* tmp) {
+                         double* tmp0) {
   const int64_t k = j2 - j1;
-  for (int64_t r = 0; r < rows; ++r) {
-    for (int64_t c = 0; c < k; ++c) {
-      double acc = 0.0;
-      for (int64_t l = 0; l < k; ++l) acc += IDX(A, lda, r, j1 + l) * V[l + c * k];
-      tmp[c] = acc;
+#ifdef _OPENMP
+#pragma omp parallel
+#endif
+  {
+#ifdef _OPENMP
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)k);
+#pragma omp for schedule(static)
+#else
+    double* tmp = tmp0;
+#endif
+    for (int64_t r = 0; r < rows; ++r) {
+      for (int64_t c = 0; c < k; ++c) {
+        double acc = 0.0;
+        for (int64_t l = 0; l < k; ++l) acc += IDX(A, lda, r, j1 + l) * V[l + c * k];
+        tmp[c] = acc;
+      }
+      for (int64_t c = 0; c < k; ++c) IDX(A, lda, r, j1 + c) = tmp[c];
     }
-    for (int64_t c = 0; c < k; ++c) IDX(A, lda, r, j1 + c) = tmp[c];
+#ifdef _OPENMP
+    free(tmp);
+#endif
   }
+  (void)tmp0;
 }
 
 int or_greorder(int mode, int64_t n, double* S, int64_t lds, double* T, int64_t ldt,

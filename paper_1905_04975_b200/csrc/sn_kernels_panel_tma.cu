@@ -52,9 +52,8 @@ struct TCfg {
   static constexpr int A_BYTES = 8 * LDA * MT;
   static constexpr int B_BYTES = 8 * (LDBR * KC > LDBL * NT ? LDBR * KC : LDBL * NT);
   static constexpr int STAGE = ((A_BYTES + B_BYTES + 1023) / 1024) * 1024;
-  static constexpr size_t SMEM = (size_t)STAGE * NS + 1024 + 2 * 8 * NS + 8 + 2 * 8 * 4 + 4 * 160;
+  static constexpr size_t SMEM = (size_t)STAGE * NS + 1024 + 2 * 8 * NS + 8;
 };
-constexpr int kMsgRing = 4;   // strip descriptors in flight from the producer to the consumers
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -109,16 +108,6 @@ struct StripInfo {
   int pk, pnk, pslot;
   int64_t pjc;
 };
-// A strip as the producer warp resolves it for the consumers (shared memory ring): the strip
-// and, per pass and consumer warp, the K interval of the warp's 32 Z^T rows (Z structure).
-// Resolving a strip is a chain of dependent global loads (binary search over the level's
-// prefix sums, the window descriptor, the status word, the Z column intervals); the producer
-// runs ahead of the consumers, so this latency is hidden instead of opening every strip.
-struct StripMsg {
-  StripInfo si;
-  int16_t lo[2][8], hi[2][8];
-};
-static_assert(sizeof(StripMsg) <= 160, "StripMsg");
 
 template <int KIND>
 __device__ __forceinline__ StripInfo resolve(const PanelArgs& a, int sid) {
@@ -190,18 +179,11 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
   uint64_t* full = (uint64_t*)(smem + (size_t)C::STAGE * C::NS);
   uint64_t* empty = full + C::NS;
   uint64_t* wb = empty + C::NS;     // fused Q passes: first pass stored (one arrival per consumer warp)
-  uint64_t* mfull = wb + 1;         // strip descriptor ring: published by the producer
-  uint64_t* mempty = mfull + kMsgRing;   // ... read by every consumer warp
-  StripMsg* msgs = (StripMsg*)(mempty + kMsgRing);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < C::NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::CONS);
-    }
-    for (int s = 0; s < kMsgRing; ++s) {
-      mbar_init(&mfull[s], 1);
-      mbar_init(&mempty[s], C::CONS);
     }
     mbar_init(wb, C::CONS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -215,43 +197,9 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
   if (warp == C::CONS) {
     // ---------------- producer: one elected lane issues every TMA
     // the whole warp walks the schedule (warp-uniform values); one elected lane issues
-    uint32_t it = 0, wbuse = 0, mi = 0;
-    for (int sid = s_begin; sid < nstrips; sid += s_step, ++mi) {
+    uint32_t it = 0, wbuse = 0;
+    for (int sid = s_begin; sid < nstrips; sid += s_step) {
       const StripInfo si = resolve<KIND>(a, sid);
-      {
-        // publish the strip and every consumer warp's K intervals (warp-uniform values; lane 0
-        // writes, its arrive releases the writes)
-        const int ms = mi % kMsgRing;
-        mbar_wait(&mempty[ms], ((mi / kMsgRing) & 1) ^ 1);
-        StripMsg* m = msgs + ms;
-        for (int p = 0; p < 2; ++p) {
-          if ((p == 0 && !si.pdo) || (p == 1 && si.skip)) continue;
-          // lane l: Z columns 8l .. 8l+7 (consumer warp l / 4), two 16-byte loads
-          const int16_t* zr = a.zrange + (int64_t)(p ? si.slot : si.pslot) * kZrange;
-          int lo = kZld, hi = -1;
-          if (lane < MT / 8) {
-            const int4 vl = *reinterpret_cast<const int4*>(zr + 8 * lane);
-            const int4 vh = *reinterpret_cast<const int4*>(zr + kZld + 8 * lane);
-            const int wl[4] = {vl.x, vl.y, vl.z, vl.w}, wh[4] = {vh.x, vh.y, vh.z, vh.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              lo = min(lo, min((int)(int16_t)(wl[q] & 0xffff), (int)(int16_t)(wl[q] >> 16)));
-              hi = max(hi, max((int)(int16_t)(wh[q] & 0xffff), (int)(int16_t)(wh[q] >> 16)));
-            }
-          }
-          lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
-          hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
-          lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
-          hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
-          if (lane < MT / 8 && (lane & 3) == 0) { m->lo[p][lane >> 2] = (int16_t)lo; m->hi[p][lane >> 2] = (int16_t)hi; }
-        }
-        __syncwarp();   // the interval writes of lanes 4w precede lane 0's release
-        if (lane == 0) {
-          m->si = si;
-          mbar_arrive(&mfull[ms]);
-        }
-        __syncwarp();
-      }
       // passes: the fused predecessor's Z (p = 0), then this window's (p = 1)
       for (int p = si.pdo ? 0 : 1; p < 2; ++p) {
       if (p == 1 && si.skip) break;
@@ -295,29 +243,26 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
   // ---------------- consumers
   const int g = lane >> 2, t = lane & 3;
   const int wm0 = warp * 32;
-  uint32_t it = 0, mi = 0;
-  for (int sid = s_begin; sid < nstrips; sid += s_step, ++mi) {
-    StripInfo si;
-    int mlo[2], mhi[2];
-    {
-      const int ms = mi % kMsgRing;
-      mbar_wait(&mfull[ms], (mi / kMsgRing) & 1);
-      const StripMsg* m = msgs + ms;
-      // field by field (a struct copy out of shared memory goes through the stack)
-      si.x0 = m->si.x0; si.j1 = m->si.j1; si.jc = m->si.jc; si.pjc = m->si.pjc;
-      si.nx = m->si.nx; si.k = m->si.k; si.nk = m->si.nk; si.pk = m->si.pk; si.pnk = m->si.pnk;
-      si.skip = m->si.skip; si.pdo = m->si.pdo;
-#pragma unroll
-      for (int p = 0; p < 2; ++p) { mlo[p] = m->lo[p][warp]; mhi[p] = m->hi[p][warp]; }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&mempty[ms]);
-    }
+  uint32_t it = 0;
+  for (int sid = s_begin; sid < nstrips; sid += s_step) {
+    const StripInfo si = resolve<KIND>(a, sid);
     for (int p = si.pdo ? 0 : 1; p < 2; ++p) {
     if (p == 1 && si.skip) break;
-    const int pk = p ? si.k : si.pk, pnk = p ? si.nk : si.pnk;
+    const int pk = p ? si.k : si.pk, pnk = p ? si.nk : si.pnk, pslot = p ? si.slot : si.pslot;
     const int64_t pjc = p ? si.jc : si.pjc;
     // K interval of this warp's 32 output rows (Z structure; exact zeros outside)
-    const int wlo = p ? mlo[1] : mlo[0], whi = p ? mhi[1] : mhi[0];
+    int wlo, whi;
+    {
+      const int16_t* zr = a.zrange + (int64_t)pslot * kZrange;
+      int lo = zr[wm0 + lane], hi = zr[kZld + wm0 + lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      wlo = lo;
+      whi = hi;
+    }
     const int boff = LEFT ? (int)(si.j1 & 1) : 0;
     double acc[2][8][4];
 #pragma unroll
@@ -334,7 +279,7 @@ __global__ void __launch_bounds__(TCfg<MT>::THREADS, 1)
 #pragma unroll
       for (int ks = 0; ks < KC; ks += 4) {
         const int kg = kc * KC + ks;
-        if (!(dbg & 64) && (kg + 3 < wlo || kg > whi)) continue;   // Z^T rows of this warp are exact zeros here (bit 64: dense)
+        if (kg + 3 < wlo || kg > whi) continue;   // Z^T rows of this warp are exact zeros here
         if (dbg & 2) continue;
         double a0[2], a1[2], bf[8];
 #pragma unroll

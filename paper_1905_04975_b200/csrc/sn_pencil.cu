@@ -24,10 +24,14 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "sn_device.cuh"
 #include "sn_exec.h"
 #include "sn_plan.h"
 #include "sn_reorder.h"
+
+namespace cg = cooperative_groups;
 
 namespace sn {
 namespace {
@@ -556,10 +560,12 @@ __device__ __forceinline__ unsigned pl_cluster_size() {
   return r;
 }
 
-// Window task on a thread-block cluster of C CTAs (C = 1: a plain CTA).  Every CTA evaluates
-// all transforms of a step (identical arithmetic, so identical records and rejection
-// decisions) and the block-size bookkeeping in its own shared memory; the row and column
-// applications -- the bulk of the work -- are split over the C x 256 threads.  Phases that
+// Window task on a thread-block cluster of C CTAs (C = 1: a plain CTA).  The transforms of a
+// step are split over the CTAs (swap i on CTA i % C), each CTA gathers the others' records
+// from distributed shared memory (the same values: the applications do not depend on which CTA
+// evaluated a transform), the block-size bookkeeping runs in every CTA's own shared memory,
+// and the row and column applications -- the bulk of the work -- are split over the C x 256
+// threads.  Phases that
 // read what another CTA wrote are separated by cluster barriers (release / acquire), and every
 // global read of the window, T, UL and VR bypasses L1 (ld.global.cg), so no CTA sees a stale
 // line of another SM's writes.
@@ -586,8 +592,11 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   __shared__ int16_t s_j[kZld];      // per swap of the current step: window row, size m
   __shared__ int8_t s_m[kZld];
   __shared__ int16_t s_lo[kZld], s_hi[kZld];   // merged nonzero row interval of its UL/VR columns
-  __shared__ int s_rej;
+  __shared__ int s_tstart[4];                  // first swap of each type in the current step
+  __shared__ int8_t s_owner[kZld];             // CTA of the cluster that evaluates each swap
+  __shared__ int s_rej, s_rejall;   // first rejected swap (list index): this CTA's, the cluster's
   __shared__ double s_why[2];
+  cg::cluster_group cl = cg::this_cluster();
   for (int64_t i = gt; i < kZslot; i += GC) {
     const int r = (int)(i % kZld), c = (int)(i / kZld);
     const double v = (r == c && c < k) ? 1.0 : 0.0;
@@ -598,7 +607,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
     zlo[tid] = (int16_t)(tid < k ? tid : kZld - 1);
     zhi[tid] = (int16_t)(tid < k ? tid : 0);
   }
-  if (tid == 0) s_rej = 0x7fffffff;
+  if (tid == 0) s_rej = s_rejall = 0x7fffffff;
   csync();
   const int64_t s0 = a.swap_off[wd.sidx];
   const int32_t* soff = a.step_off + a.step_base[wd.sidx];
@@ -611,29 +620,85 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   };
   for (int st = 0; st < nsteps; ++st) {
     const int b0 = soff[st], cnt = soff[st + 1] - b0;
-    // (1) transforms, one thread per swap
-    if (tid < cnt) {
-      const int64_t s = s0 + b0 + tid;
-      const int j = a.sj[s], n1 = a.s12[s] >> 4, n2 = a.s12[s] & 15;
-      s_j[tid] = (int16_t)j;
-      s_m[tid] = (int8_t)(n1 + n2);
-      double* R = rec + tid * kRecD;
-      double why[2] = {0.0, 0.0};
-      bool ok;
-      if (n1 == 1 && n2 == 1) ok = pl_transform<1, 1>(Sw, ldS, Tw, ldT, j, R, why);
-      else if (n1 == 1) ok = pl_transform<1, 2>(Sw, ldS, Tw, ldT, j, R, why);
-      else if (n2 == 1) ok = pl_transform<2, 1>(Sw, ldS, Tw, ldT, j, R, why);
-      else ok = pl_transform<2, 2>(Sw, ldS, Tw, ldT, j, R, why);
-      if (wd.order == a.force_order && a.sidx[s] == a.force_swap) { ok = false; why[0] = 0.0; }
-      if (ok && rank == 0) atomicMax(&a.ctl->ratio_bits, (unsigned long long)__double_as_longlong(why[1]));
-      if (!ok) {
-        const int key = a.sidx[s];
-        if (atomicMin(&s_rej, key) > key) { s_why[0] = why[0]; s_why[1] = why[1]; }
+    // (1) transforms, one thread per swap.  The step's swaps are sorted by type (host); a warp
+    // takes up to 32 swaps of ONE type (a warp running several specialisations of the
+    // transform would run them one after the other), and the warp tasks are spread over the
+    // cluster's CTAs first (task g on CTA g % C, warp g / C).
+    if (tid < 4) s_tstart[tid] = cnt;
+    __syncthreads();
+    for (int i = tid; i < cnt; i += blockDim.x) {
+      const int64_t s = s0 + b0 + i;
+      const int8_t v = a.s12[s];
+      s_j[i] = (int16_t)a.sj[s];
+      s_m[i] = (int8_t)((v >> 4) + (v & 15));
+      const int ty = ((v >> 4) - 1) * 2 + ((v & 15) - 1);
+      int tp = -1;
+      if (i > 0) { const int8_t u = a.s12[s - 1]; tp = ((u >> 4) - 1) * 2 + ((u & 15) - 1); }
+      for (int t = tp + 1; t <= ty; ++t) s_tstart[t] = i;   // first swap of type >= t
+    }
+    __syncthreads();
+    int tbase[5];                                      // first warp task of each type
+    tbase[0] = 0;
+    for (int t = 0; t < 4; ++t) tbase[t + 1] = tbase[t] + (((t < 3 ? s_tstart[t + 1] : cnt) - s_tstart[t] + 31) >> 5);
+    for (int i = tid; i < cnt; i += blockDim.x) {
+      int t = 0;
+      while (t < 3 && s_tstart[t + 1] <= i) ++t;
+      s_owner[i] = (int8_t)((tbase[t] + ((i - s_tstart[t]) >> 5)) % (int)C);
+    }
+    for (int g = (tid >> 5) * (int)C + (int)rank; g < tbase[4]; g += (int)(C * (blockDim.x >> 5))) {
+      int t = 0;
+      while (t < 3 && tbase[t + 1] <= g) ++t;
+      const int i = s_tstart[t] + ((g - tbase[t]) << 5) + (tid & 31);
+      if (i < (t < 3 ? s_tstart[t + 1] : cnt)) {
+        const int64_t s = s0 + b0 + i;
+        const int j = a.sj[s], n1 = a.s12[s] >> 4, n2 = a.s12[s] & 15;
+        double* R = rec + i * kRecD;
+        double why[2] = {0.0, 0.0};
+        bool ok;
+        const long long tq0 = a.pprof ? clock64() : 0;
+        if (n1 == 1 && n2 == 1) ok = pl_transform<1, 1>(Sw, ldS, Tw, ldT, j, R, why);
+        else if (n1 == 1) ok = pl_transform<1, 2>(Sw, ldS, Tw, ldT, j, R, why);
+        else if (n2 == 1) ok = pl_transform<2, 1>(Sw, ldS, Tw, ldT, j, R, why);
+        else ok = pl_transform<2, 2>(Sw, ldS, Tw, ldT, j, R, why);
+        if (a.pprof) {   // per-type transform latency (sum, count)
+          const int ty = (n1 - 1) * 2 + (n2 - 1);
+          atomicAdd(&a.pprof[8 + ty], (unsigned long long)(clock64() - tq0));
+          atomicAdd(&a.pprof[12 + ty], 1ull);
+        }
+        if (wd.order == a.force_order && a.sidx[s] == a.force_swap) { ok = false; why[0] = 0.0; }
+        if (ok) atomicMax(&a.ctl->ratio_bits, (unsigned long long)__double_as_longlong(why[1]));
+        if (!ok) {
+          const int key = a.sidx[s];
+          if (atomicMin(&s_rej, key) > key) { s_why[0] = why[0]; s_why[1] = why[1]; }
+        }
       }
     }
-    csync();   // every CTA has read the diagonal blocks before any is overwritten
+    csync();   // every transform is done (and every diagonal block read) before any is overwritten
+    if (C > 1) {
+      // gather the records the other CTAs computed (distributed shared memory) and the
+      // cluster-wide first rejection
+      for (int q = tid; q < cnt * kRecD; q += blockDim.x) {
+        const unsigned owner = (unsigned)s_owner[q / kRecD];
+        if (owner != rank) rec[q] = cl.map_shared_rank(rec, owner)[q];
+      }
+      if (tid == 0) {
+        int best = s_rej;
+        for (unsigned r = 0; r < C; ++r) best = min(best, *cl.map_shared_rank(&s_rej, r));
+        if (best != 0x7fffffff && rank == 0 && s_rej != best)
+          for (unsigned r = 1; r < C; ++r)
+            if (*cl.map_shared_rank(&s_rej, r) == best) {
+              s_why[0] = cl.map_shared_rank(s_why, r)[0];
+              s_why[1] = cl.map_shared_rank(s_why, r)[1];
+            }
+        s_rejall = best;
+      }
+      __syncthreads();
+    } else if (tid == 0) {
+      s_rejall = s_rej;
+    }
+    __syncthreads();
     ptick(0);
-    if (s_rej != 0x7fffffff) break;
+    if (s_rejall != 0x7fffffff) break;
     // (2) column intervals of the accumulators; row-application task counts
     if (tid < cnt) {
       const int j = s_j[tid], m = s_m[tid];
@@ -748,6 +813,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   }
   const int done = soff[done_steps] - soff[0];
   const int total = soff[nsteps] - soff[0];
+  csync();   // no CTA leaves while another may still read its shared memory
   if (rank != 0) return;
   if (tid < kZld) {
     int16_t* zr = a.zrange + (int64_t)wd.slot * kZrange;
@@ -957,8 +1023,8 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
     if (Q) panel_maps_init(&mQ, (double*)dUL.p, maxper, Q, n, n, ldQ);
     if (Zm) panel_maps_init(&mZ, (double*)dVR.p, maxper, Zm, n, n, ldZ);
     if (std::getenv("SN_PPROF")) {
-      PK(dpprof.alloc(8 * sizeof(unsigned long long)));
-      PK(cudaMemsetAsync(dpprof.p, 0, 8 * sizeof(unsigned long long), sA));
+      PK(dpprof.alloc(16 * sizeof(unsigned long long)));
+      PK(cudaMemsetAsync(dpprof.p, 0, 16 * sizeof(unsigned long long), sA));
     }
     PK(cudaEventCreate(&e0));
     PK(cudaEventCreate(&e1));
@@ -1045,14 +1111,18 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
     PK(cudaMemcpy(hdone.data(), ddone.p, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
     PK(cudaMemcpy(&hctl, dctl.p, sizeof(Control), cudaMemcpyDeviceToHost));
     if (dpprof.p) {
-      unsigned long long h[8];
+      unsigned long long h[16];
       PK(cudaMemcpy(h, dpprof.p, sizeof(h), cudaMemcpyDeviceToHost));
       const double w = h[5] ? (double)h[5] : 1.0;
+      double lat[4];
+      for (int q = 0; q < 4; ++q) lat[q] = h[12 + q] ? (double)h[8 + q] / (double)h[12 + q] : 0.0;
       std::fprintf(stderr,
                    "{\"probe\": \"pencil_window_phases\", \"windows\": %llu, \"steps_per_window\": %.1f, "
                    "\"swaps_per_window\": %.1f, \"cycles_per_window\": {\"transform\": %.0f, \"intervals\": %.0f, "
-                   "\"rows\": %.0f, \"cols\": %.0f}}\n",
-                   h[5], h[4] / w, h[6] / w, h[0] / w, h[1] / w, h[2] / w, h[3] / w);
+                   "\"rows\": %.0f, \"cols\": %.0f}, \"transform_cycles_by_type\": [%.0f, %.0f, %.0f, %.0f], "
+                   "\"swaps_by_type\": [%llu, %llu, %llu, %llu]}\n",
+                   h[5], h[4] / w, h[6] / w, h[0] / w, h[1] / w, h[2] / w, h[3] / w, lat[0], lat[1], lat[2], lat[3],
+                   h[12], h[13], h[14], h[15]);
     }
   }
   {
@@ -1137,10 +1207,47 @@ extern "C" int sn_reorder_pencil_ex(const sn_opts* opts, int64_t n, double* S, i
   if (Z && ldZ < n) return -10;
   if (!select) return -11;
   if (o.window < 4 || o.window > 256 || o.inner_window < 4 || o.inner_window > kInner) return SN_ERR_UNSUPPORTED;
-  if (!is_device_ptr(S) || !is_device_ptr(T) || (Q && !is_device_ptr(Q)) || (Z && !is_device_ptr(Z)))
-    return SN_ERR_UNSUPPORTED;   // device pointers only (this version)
   std::lock_guard<std::mutex> lock(g_mu);
   sn_stats local;
   sn_stats* st = stats ? stats : &local;
-  return run_pencil(o, n, S, ldS, T, ldT, Q, ldQ, Z, ldZ, select, m, bmap_out, st, (cudaStream_t)stream);
+  cudaStream_t sA = (cudaStream_t)stream;
+  // Host buffers: each host matrix is staged through a compact (ld = n) device copy, copied
+  // in before the call and back after it (also after SN_ERR_REJECTED: a valid partial form).
+  double* user[4] = {S, T, Q, Z};
+  const int64_t uld[4] = {ldS, ldT, ldQ, ldZ};
+  double* dev[4] = {S, T, Q, Z};
+  int64_t dld[4] = {ldS, ldT, ldQ, ldZ};
+  DevBuf stage[4];
+  bool staged = false;
+  double h2d = 0.0;
+  for (int i = 0; i < 4; ++i) {
+    if (!user[i] || is_device_ptr(user[i])) continue;
+    const double t = now_ms();
+    if (stage[i].alloc(sizeof(double) * (size_t)n * (size_t)n) != cudaSuccess) return SN_ERR_CUDA;
+    if (cudaMemcpy2DAsync(stage[i].p, sizeof(double) * n, user[i], sizeof(double) * uld[i], sizeof(double) * n, n,
+                          cudaMemcpyHostToDevice, sA) != cudaSuccess)
+      return SN_ERR_CUDA;
+    dev[i] = (double*)stage[i].p;
+    dld[i] = n;
+    staged = true;
+    if (cudaStreamSynchronize(sA) != cudaSuccess) return SN_ERR_CUDA;
+    h2d += now_ms() - t;
+  }
+  int rc = run_pencil(o, n, dev[0], dld[0], dev[1], dld[1], dev[2], dld[2], dev[3], dld[3], select, m, bmap_out, st,
+                      sA);
+  if (staged) {
+    st->ms_h2d = h2d;
+    if (rc == SN_OK || rc == SN_ERR_REJECTED) {
+      const double t = now_ms();
+      for (int i = 0; i < 4; ++i) {
+        if (!stage[i].p) continue;
+        if (cudaMemcpy2DAsync(user[i], sizeof(double) * uld[i], stage[i].p, sizeof(double) * n, sizeof(double) * n, n,
+                              cudaMemcpyDeviceToHost, sA) != cudaSuccess)
+          return SN_ERR_CUDA;
+      }
+      if (cudaStreamSynchronize(sA) != cudaSuccess) return SN_ERR_CUDA;
+      st->ms_d2h = now_ms() - t;
+    }
+  }
+  return rc;
 }

@@ -11,6 +11,8 @@ properties that hold at any size (north_star invariants):
 plus, for config 3, prefix parity with the oracle (the first 32 windows on both sides, >= 3 DAG
 levels, all of S and Q compared elementwise within 1e-9 ||S||_F).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -84,7 +86,10 @@ def _run_fullsize(cfg, prefix_windows=0, min_levels=1):
         torch.cuda.synchronize()
         # the prefix must exercise the multi-level executor (lookahead strips, Q overlap)
         assert got["stats"]["levels"] >= min_levels, got["stats"]["levels"]
-        ref = oracle.reorder(S0h, Q0h, p.select, w=p.w, mode=1, max_windows=prefix_windows, inplace=True)
+        # the oracle's panel rows / columns on the host's cores (bitwise the one-thread result,
+        # tests/test_oracle_pins.py): the same arithmetic, minutes less of the GPU suite
+        ref = oracle.reorder_threads(S0h, Q0h, p.select, w=p.w, threads=os.cpu_count() or 1,
+                                     max_windows=prefix_windows, inplace=True)
         assert got["rc"] == 0 == ref["rc"]
         np.testing.assert_array_equal(got["bmap"], ref["bmap"])
         nS = float(torch.linalg.norm(S).item())
@@ -158,7 +163,8 @@ def test_config4_prefix_parity_sampled_Q():
     got = sn.reorder(S, Q, p.select, window=p.w, max_windows=K)
     torch.cuda.synchronize()
     assert got["rc"] == 0 and got["stats"]["windows"] == K
-    ref = oracle.reorder(S0h, Q0s, p.select, w=p.w, mode=1, max_windows=K, inplace=True)
+    ref = oracle.reorder_threads(S0h, Q0s, p.select, w=p.w, threads=os.cpu_count() or 1, max_windows=K,
+                                 inplace=True)
     assert ref["rc"] == 0 and ref["stats"]["windows"] == K
     np.testing.assert_array_equal(got["bmap"], ref["bmap"])
     dS = 0.0

@@ -6,6 +6,8 @@ the swaps of a window in a different (commuting) order than the oracle (inner wi
 DESIGN.md §4), so agreement is to rounding, far inside the bar; the measured maxima are
 printed.  Inputs come from workloads/ only; expected values only from oracle/.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -25,11 +27,16 @@ def built():
     assert torch.cuda.is_available()
 
 
-def run_both(p, w=None, q=True, **opts):
+def run_both(p, w=None, q=True, oracle_threads=0, **opts):
     w = w or p.w
     S0 = p.S_np().copy(order="F")
     Q0 = p.Q_np().copy(order="F") if (q and p.Q is not None) else None
-    ref = oracle.reorder(S0, Q0, p.select, w=w, mode=1)
+    if oracle_threads:
+        # the oracle's panel rows / columns on the host's cores: bitwise the one-thread result
+        # (tests/test_oracle_pins.py), minutes less of the GPU suite at n = 4096
+        ref = oracle.reorder_threads(S0, Q0, p.select, w, oracle_threads)
+    else:
+        ref = oracle.reorder(S0, Q0, p.select, w=w, mode=1)
     S = p.S.cuda().contiguous()
     Q = p.Q.cuda().contiguous() if Q0 is not None else None
     got = sn.reorder(S, Q, p.select, window=w, validate_lower=1, **opts)
@@ -82,7 +89,7 @@ def test_config1_parity():
     """BASELINE config 1 (n = 4096, w = 128, random orthogonal Q), full oracle run."""
     p = make_config(1, seed=1, device="cuda")
     p.S = p.S.cpu(); p.Q = p.Q.cpu()
-    S0, Q0, ref, got, Sg, Qg = run_both(p)
+    S0, Q0, ref, got, Sg, Qg = run_both(p, oracle_threads=os.cpu_count() or 1)
     assert_parity(S0, Q0, ref, got, Sg, Qg, "config1")
     check_reordering(S0, Q0, p.select, Sg, Qg, got["select"], got["m"], got["bmap"])
 
@@ -200,7 +207,7 @@ def test_prefix_parity_config2():
     Q0 = np.asfortranarray(p.Q.cpu().numpy().T)
     S, Q = p.S.clone(), p.Q.clone()
     got = sn.reorder(S, Q, p.select, window=p.w, max_windows=K)
-    ref = oracle.reorder(S0, Q0, p.select, w=p.w, mode=1, max_windows=K)
+    ref = oracle.reorder_threads(S0, Q0, p.select, p.w, os.cpu_count() or 1, max_windows=K)
     assert got["rc"] == 0 == ref["rc"]
     assert got["stats"]["windows"] == ref["stats"]["windows"] == K
     np.testing.assert_array_equal(got["bmap"], ref["bmap"])

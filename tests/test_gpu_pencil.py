@@ -8,6 +8,8 @@ in-window swap order differs, reading R12, so agreement is to rounding; the basi
 convention G7 makes the signs a function of the data, not of rounding-level choices such as
 which re-triangularisation G2 keeps), and the invariants of a generalized reordering.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -47,9 +49,9 @@ def _run(p, window, with_q=True, with_z=True, **opts):
     return (S, T, Q, Z), r
 
 
-def _compare(p, window, **kw):
+def _compare(p, window, oracle_threads=0, **kw):
     (S, T, Q, Z), r = _run(p, window, **kw)
-    ref = oracle.greorder(S, T, Q, Z, p.select, w=window, mode=1)
+    ref = oracle.greorder(S, T, Q, Z, p.select, w=window, mode=1, threads=oracle_threads)
     assert r["rc"] == 0 == ref["rc"]
     assert r["m"] == ref["m"]
     np.testing.assert_array_equal(r["bmap"], ref["bmap"])
@@ -81,7 +83,7 @@ def test_pencil_matches_oracle(n, p2, w, psel, seed):
 def test_pencil_config1_size():
     # config-1 shape (n = 4096, w = 128, 25 % 2x2 blocks, Bernoulli(0.35)) as a pencil
     p = make_pencil(4096, p2=0.25, q="householder", psel=0.35, w=128, seed=1)
-    r = _compare(p, 128)
+    r = _compare(p, 128, oracle_threads=os.cpu_count() or 1)   # bitwise the one-thread oracle
     print("pencil n=4096: windows=%d levels=%d swaps=%d ms_device=%.1f"
           % (r["stats"]["windows"], r["stats"]["levels"], r["stats"]["swaps"], r["stats"]["ms_device"]))
 
@@ -179,7 +181,7 @@ def test_pencil_config2_size_completes_with_prefix_parity():
     dS, dT, dQ, dZ = _dev(S), _dev(T), _dev(Q), _dev(Z)
     r = sn.reorder_pencil(dS, dT, dQ, dZ, p.select, window=256, max_windows=K)
     torch.cuda.synchronize()
-    ref = oracle.greorder(S, T, Q, Z, p.select, w=256, mode=1, max_windows=K)
+    ref = oracle.greorder(S, T, Q, Z, p.select, w=256, mode=1, max_windows=K, threads=os.cpu_count() or 1)
     assert r["rc"] == 0 == ref["rc"] and r["stats"]["windows"] == K == ref["stats"]["windows"]
     np.testing.assert_array_equal(r["bmap"], ref["bmap"])
     nS = np.linalg.norm(S)
@@ -233,3 +235,38 @@ def test_pencil_cluster_forced_rejection_bitwise():
     assert r1["stats"]["rejected_window"] == r4["stats"]["rejected_window"] == 3
     for key in ("S", "T", "Q", "Z"):
         np.testing.assert_array_equal(r4[key], r1[key])
+
+
+def test_pencil_host_buffers_match_device_buffers():
+    """Host (pageable) S, T, Q, Z are staged through device copies inside the call: bitwise the
+    device-buffer result, for a padded leading dimension too (through the raw C ABI)."""
+    p = make_pencil(333, p2=0.25, q="householder", psel=0.4, w=64, seed=13)
+    (S, T, Q, Z), rd = _run(p, 64)
+    assert rd["rc"] == 0
+    hs = [torch.as_tensor(np.ascontiguousarray(X.T)) for X in (S, T, Q, Z)]   # CPU tensors
+    rh = sn.reorder_pencil(*hs, p.select, window=64)
+    assert rh["rc"] == 0 and rh["m"] == rd["m"]
+    assert rh["stats"]["ms_h2d"] > 0 and rh["stats"]["ms_d2h"] > 0
+    for key, t in zip(("S", "T", "Q", "Z"), hs):
+        np.testing.assert_array_equal(t.numpy().T, rd[key], err_msg=key)
+    np.testing.assert_array_equal(rh["bmap"], rd["bmap"])
+    # ld = n + 3 (column-major with padding), Q absent, through the C ABI
+    import ctypes as C
+    n, ld = S.shape[0], S.shape[0] + 3
+    pads = []
+    for X in (S, T, Z):
+        A = np.zeros((ld, n), order="F")
+        A[:n, :] = X
+        pads.append(A)
+    o = sn.default_opts(window=64)
+    sel = np.ascontiguousarray(p.select, np.int32).copy()
+    m = C.c_int64()
+    bm = np.zeros(n, np.int8)
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)
+    rc = sn.lib().sn_reorder_pencil_ex(C.byref(o), n, ptr(pads[0]), ld, ptr(pads[1]), ld, None, n, ptr(pads[2]), ld,
+                                       ptr(sel), C.byref(m), ptr(bm), None, None)
+    (_, _, _, _), rn = _run(p, 64, with_q=False)
+    assert rc == 0 == rn["rc"]
+    np.testing.assert_array_equal(pads[0][:n], rn["S"])
+    np.testing.assert_array_equal(pads[1][:n], rn["T"])
+    np.testing.assert_array_equal(pads[2][:n], rn["Z"])

@@ -375,3 +375,18 @@ def test_greorder_inwindow_order_independence():
     assert np.abs(S - dQ[:, None] * ref["S"] * dZ[None, :]).max() <= 1e-11 * np.linalg.norm(S)
     assert np.abs(T - dQ[:, None] * ref["T"] * dZ[None, :]).max() <= 1e-11 * np.linalg.norm(T)
     assert np.abs(Q - ref["Q"] * dQ).max() <= 1e-11 and np.abs(Z - ref["Z"] * dZ).max() <= 1e-11
+
+
+def test_greorder_threaded_is_bitwise_the_oracle():
+    """The -fopenmp build of or_greorder (used by the GPU tests at the config-1/2 pencil sizes)
+    runs the same code, every panel row / column keeping its summation order: bitwise the
+    one-thread result, with and without a window prefix."""
+    p = make_pencil(420, p2=0.25, q="householder", psel=0.4, w=64, seed=17)
+    S, T, Q, Z = p.np("S"), p.np("T"), p.np("Q"), p.np("Z")
+    for mw in (-1, 5):
+        a = oracle.greorder(S, T, Q, Z, p.select, w=64, max_windows=mw)
+        b = oracle.greorder(S, T, Q, Z, p.select, w=64, max_windows=mw, threads=3)
+        assert a["rc"] == b["rc"] == 0
+        for key in ("S", "T", "Q", "Z"):
+            assert np.array_equal(a[key], b[key]), key
+        np.testing.assert_array_equal(a["bmap"], b["bmap"])

@@ -521,3 +521,16 @@ def test_threaded_oracle_is_bitwise_the_oracle():
     assert a["rc"] == b["rc"] == 0
     assert np.array_equal(a["S"], b["S"]) and np.array_equal(a["Q"], b["Q"])
     np.testing.assert_array_equal(a["bmap"], b["bmap"])
+
+
+def test_threaded_oracle_prefix_and_q_sample_bitwise():
+    """reorder_threads with max_windows and a row sample of Q (the GPU full-size prefix tests'
+    arguments) is bitwise reorder() with the same arguments."""
+    p = make_problem(600, p2=0.5, q="householder", psel=0.35, w=64, seed=43)
+    S0, Q0 = p.S_np().copy(order="F"), p.Q_np().copy(order="F")
+    rows = np.array([1, 44, 300, 599])
+    for Qa in (Q0, np.asfortranarray(Q0[rows])):
+        a = oracle.reorder(S0, Qa, p.select, w=64, max_windows=7)
+        b = oracle.reorder_threads(S0, Qa, p.select, 64, 3, max_windows=7)
+        assert a["rc"] == b["rc"] == 0 and a["stats"]["windows"] == 7
+        assert np.array_equal(a["S"], b["S"]) and np.array_equal(a["Q"], b["Q"])
