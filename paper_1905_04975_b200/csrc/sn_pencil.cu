@@ -282,6 +282,90 @@ __host__ __device__ __forceinline__ bool pl_std_t22(const double* Tb, double* P,
   return p2r * w0 + p2c * w1 > 0.0;
 }
 
+// G4 and G7 on a swap's accepted transform: the new blocks below the leading one set to zero,
+// T's 2x2 blocks diagonal (2x2 SVD), moved 1x1 blocks with t >= 0, the sign convention.
+template <int N1, int N2>
+__host__ __device__ __forceinline__ bool pl_swap_tail(double* U, double* V, double* An, double* Bn, double* why) {
+  constexpr int n1 = N1, n2 = N2, m = N1 + N2;
+#pragma unroll
+  for (int c = 0; c < n2; ++c)
+#pragma unroll
+    for (int r = n2; r < m; ++r) { An[r + 4 * c] = 0.0; Bn[r + 4 * c] = 0.0; }
+  // G4: 2x2 blocks
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    int p = -1;
+    if (q == 0 && n2 == 2) p = 0;
+    if (q == 1 && n1 == 2) p = n2;
+    if (p < 0) continue;
+    const double Tb[4] = {Bn[p + 4 * p], Bn[(p + 1) + 4 * p], Bn[p + 4 * (p + 1)], Bn[(p + 1) + 4 * (p + 1)]};
+    double P2[4], W2[4];
+    if (!pl_std_t22(Tb, P2, W2)) {
+      if (why) { why[0] = 2.0; why[1] = 0.0; }
+      return false;
+    }
+    double Pm[16], Wm[16];
+    pl_eye(Pm, m);
+    pl_eye(Wm, m);
+    Pm[p + 4 * p] = P2[0]; Pm[(p + 1) + 4 * p] = P2[1]; Pm[p + 4 * (p + 1)] = P2[2]; Pm[(p + 1) + 4 * (p + 1)] = P2[3];
+    Wm[p + 4 * p] = W2[0]; Wm[(p + 1) + 4 * p] = W2[1]; Wm[p + 4 * (p + 1)] = W2[2]; Wm[(p + 1) + 4 * (p + 1)] = W2[3];
+    double A2[16], B2[16];
+    pl_congr(Pm, An, Wm, A2, m);
+    pl_congr(Pm, Bn, Wm, B2, m);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) { An[i] = A2[i]; Bn[i] = B2[i]; }
+    Bn[(p + 1) + 4 * p] = 0.0;
+    Bn[p + 4 * (p + 1)] = 0.0;
+    pl_mulr(U, Pm, m);
+    pl_mulr(V, Wm, m);
+    const double t11 = Bn[p + 4 * p], t22 = Bn[(p + 1) + 4 * (p + 1)];
+    const double e11 = An[p + 4 * p] / t11, e12 = An[p + 4 * (p + 1)] / t11;
+    const double e21 = An[(p + 1) + 4 * p] / t22, e22 = An[(p + 1) + 4 * (p + 1)] / t22;
+    const double h = 0.5 * (e11 - e22);
+    if (!(h * h + e12 * e21 < 0.0)) {
+      if (why) { why[0] = 3.0; why[1] = h * h + e12 * e21; }
+      return false;
+    }
+  }
+  // G4: moved 1x1 blocks with t >= 0
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    int p = -1;
+    if (q == 0 && n2 == 1) p = 0;
+    if (q == 1 && n1 == 1) p = n2;
+    if (p < 0 || !(Bn[p + 4 * p] < 0.0)) continue;
+#pragma unroll
+    for (int c = 0; c < m; ++c) { An[p + 4 * c] = -An[p + 4 * c]; Bn[p + 4 * c] = -Bn[p + 4 * c]; }
+#pragma unroll
+    for (int r = 0; r < m; ++r) U[r + 4 * p] = -U[r + 4 * p];
+  }
+  // G7: the largest-magnitude entry (the first such) of every column of V is positive; U's
+  // column follows, the blocks change as D An D, D Bn D
+  double d[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    int im = 0;
+#pragma unroll
+    for (int r = 1; r < m; ++r)
+      if (fabs(V[r + 4 * c]) > fabs(V[im + 4 * c])) im = r;
+    double vm = V[4 * c];
+#pragma unroll
+    for (int r = 1; r < m; ++r)
+      if (r == im) vm = V[r + 4 * c];
+    d[c] = (c < m && vm < 0.0) ? -1.0 : 1.0;
+  }
+#pragma unroll
+  for (int c = 0; c < m; ++c)
+#pragma unroll
+    for (int r = 0; r < m; ++r) {
+      U[r + 4 * c] *= d[c];
+      V[r + 4 * c] *= d[c];
+      An[r + 4 * c] *= d[r] * d[c];
+      Bn[r + 4 * c] *= d[r] * d[c];
+    }
+  return true;
+}
+
 // The transform of one swap (G1-G4, G7).  A, B: the m x m blocks of S and T (ld 4, m = n1 + n2).
 // Out: U, V (m x m), An = U^T A V, Bn = U^T B V in standard form.  Returns false = rejected.
 template <int N1, int N2>
@@ -395,83 +479,130 @@ __host__ __device__ __forceinline__ bool pl_swap_t(const double* A, const double
     }
     if (why) { why[0] = 0.0; why[1] = fmax(resA / thA, resB / thB); }
   }
+  return pl_swap_tail<N1, N2>(U, V, An, Bn, why);
+}
+
+
+// The same transform for N1 + N2 >= 3 by a group of 4 lanes (all 32 lanes of the warp call it;
+// role = lane & 3), with the same arithmetic on every value it produces (so the same record as
+// pl_swap_t): the Sylvester pair on every lane; the two Sylvester bases V0 (even lanes) and U0
+// (odd lanes), exchanged; the two re-triangularisations Uq (even) and Vr (odd) -- each one
+// congruence and one QR -- exchanged; the three G3 candidates on roles 0, 1, 2; the winner's
+// blocks by shuffle; then G4 / G7 on every lane.  Critical path: one Sylvester solve, two QRs,
+// three congruences instead of one Sylvester solve, four QRs and nine congruences.
+__device__ __forceinline__ void pl_xchg16(const double* mine, double* other, int lane) {
 #pragma unroll
-  for (int c = 0; c < n2; ++c)
-#pragma unroll
-    for (int r = n2; r < m; ++r) { An[r + 4 * c] = 0.0; Bn[r + 4 * c] = 0.0; }
-  // G4: 2x2 blocks
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    int p = -1;
-    if (q == 0 && n2 == 2) p = 0;
-    if (q == 1 && n1 == 2) p = n2;
-    if (p < 0) continue;
-    const double Tb[4] = {Bn[p + 4 * p], Bn[(p + 1) + 4 * p], Bn[p + 4 * (p + 1)], Bn[(p + 1) + 4 * (p + 1)]};
-    double P2[4], W2[4];
-    if (!pl_std_t22(Tb, P2, W2)) {
-      if (why) { why[0] = 2.0; why[1] = 0.0; }
-      return false;
-    }
-    double Pm[16], Wm[16];
-    pl_eye(Pm, m);
-    pl_eye(Wm, m);
-    Pm[p + 4 * p] = P2[0]; Pm[(p + 1) + 4 * p] = P2[1]; Pm[p + 4 * (p + 1)] = P2[2]; Pm[(p + 1) + 4 * (p + 1)] = P2[3];
-    Wm[p + 4 * p] = W2[0]; Wm[(p + 1) + 4 * p] = W2[1]; Wm[p + 4 * (p + 1)] = W2[2]; Wm[(p + 1) + 4 * (p + 1)] = W2[3];
-    double A2[16], B2[16];
-    pl_congr(Pm, An, Wm, A2, m);
-    pl_congr(Pm, Bn, Wm, B2, m);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) { An[i] = A2[i]; Bn[i] = B2[i]; }
-    Bn[(p + 1) + 4 * p] = 0.0;
-    Bn[p + 4 * (p + 1)] = 0.0;
-    pl_mulr(U, Pm, m);
-    pl_mulr(V, Wm, m);
-    const double t11 = Bn[p + 4 * p], t22 = Bn[(p + 1) + 4 * (p + 1)];
-    const double e11 = An[p + 4 * p] / t11, e12 = An[p + 4 * (p + 1)] / t11;
-    const double e21 = An[(p + 1) + 4 * p] / t22, e22 = An[(p + 1) + 4 * (p + 1)] / t22;
-    const double h = 0.5 * (e11 - e22);
-    if (!(h * h + e12 * e21 < 0.0)) {
-      if (why) { why[0] = 3.0; why[1] = h * h + e12 * e21; }
-      return false;
-    }
-  }
-  // G4: moved 1x1 blocks with t >= 0
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    int p = -1;
-    if (q == 0 && n2 == 1) p = 0;
-    if (q == 1 && n1 == 1) p = n2;
-    if (p < 0 || !(Bn[p + 4 * p] < 0.0)) continue;
-#pragma unroll
-    for (int c = 0; c < m; ++c) { An[p + 4 * c] = -An[p + 4 * c]; Bn[p + 4 * c] = -Bn[p + 4 * c]; }
-#pragma unroll
-    for (int r = 0; r < m; ++r) U[r + 4 * p] = -U[r + 4 * p];
-  }
-  // G7: the largest-magnitude entry (the first such) of every column of V is positive; U's
-  // column follows, the blocks change as D An D, D Bn D
-  double d[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    int im = 0;
-#pragma unroll
-    for (int r = 1; r < m; ++r)
-      if (fabs(V[r + 4 * c]) > fabs(V[im + 4 * c])) im = r;
-    double vm = V[4 * c];
-#pragma unroll
-    for (int r = 1; r < m; ++r)
-      if (r == im) vm = V[r + 4 * c];
-    d[c] = (c < m && vm < 0.0) ? -1.0 : 1.0;
-  }
+  for (int i = 0; i < 16; ++i) other[i] = __shfl_sync(0xffffffffu, mine[i], lane ^ 1);
+}
+
+template <int N1, int N2>
+__device__ bool pl_swap_lanes(const double* A, const double* B, double* U, double* V, double* An, double* Bn,
+                              double* why, int lane, unsigned long long* prof = nullptr) {
+  constexpr int n1 = N1, n2 = N2, m = N1 + N2;
+  // debug (SN_PPROF): cycles to the end of the Sylvester solve, the bases, the candidates, all
+  const long long k0 = prof ? clock64() : 0;
+  auto mark = [&](int q) { if (prof && lane == 0) atomicAdd(&prof[q], (unsigned long long)(clock64() - k0)); };
+  const int role = lane & 3, odd = lane & 1, gbase = lane & ~3;
+  double anorm = 0.0, bnorm = 0.0;
 #pragma unroll
   for (int c = 0; c < m; ++c)
 #pragma unroll
     for (int r = 0; r < m; ++r) {
-      U[r + 4 * c] *= d[c];
-      V[r + 4 * c] *= d[c];
-      An[r + 4 * c] *= d[r] * d[c];
-      Bn[r + 4 * c] *= d[r] * d[c];
+      anorm = fma(A[r + 4 * c], A[r + 4 * c], anorm);
+      bnorm = fma(B[r + 4 * c], B[r + 4 * c], bnorm);
     }
-  return true;
+  anorm = sqrt(anorm);
+  bnorm = sqrt(bnorm);
+  const double eps = 2.220446049250313e-16, sml = 2.2250738585072014e-308 / 2.220446049250313e-16;
+  const double thA = fmax(kG3C * eps * anorm, sml), thB = fmax(kG3C * eps * bnorm, sml);
+  double R[4] = {0.0, 0.0, 0.0, 0.0}, L[4] = {0.0, 0.0, 0.0, 0.0};
+  pl_gsylv<N1, N2>(A, B, R, L);
+  mark(0);
+  // Sylvester bases: even lanes V0 = basis of span[-R; I], odd lanes U0 = basis of span[-L; I]
+  double M[16], X[16], Y[16], U0[16], V0[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) M[i] = 0.0;
+#pragma unroll
+  for (int c = 0; c < n2; ++c) {
+#pragma unroll
+    for (int r = 0; r < n1; ++r) M[r + 4 * c] = -(odd ? L[r + 2 * c] : R[r + 2 * c]);
+    M[(n1 + c) + 4 * c] = 1.0;
+  }
+  pl_qr_basis(M, m, n2, X);
+  pl_xchg16(X, Y, lane);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { V0[i] = odd ? Y[i] : X[i]; U0[i] = odd ? X[i] : Y[i]; }
+  // re-triangularisations: even lanes Uq from the QR of (T V0)(:, 1:n2); odd lanes Vr completing
+  // the row space of (U0^T T)(n2+1:m, :)
+  double I4[16], Ua[16], Va[16], W[16];
+  pl_eye(I4, m);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { Ua[i] = odd ? U0[i] : I4[i]; Va[i] = odd ? I4[i] : V0[i]; }
+  pl_congr(Ua, B, Va, W, m);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) M[i] = 0.0;
+  if (odd) {
+#pragma unroll
+    for (int c = 0; c < n1; ++c)
+#pragma unroll
+      for (int r = 0; r < m; ++r) M[r + 4 * c] = W[(n2 + c) + 4 * r];
+    pl_qr_basis(M, m, n1, X);
+  } else {
+#pragma unroll
+    for (int c = 0; c < n2; ++c)
+#pragma unroll
+      for (int r = 0; r < m; ++r) M[r + 4 * c] = W[r + 4 * c];
+    pl_qr_basis(M, m, n2, X);
+  }
+  if (odd) {   // Vr: H's last n2 columns, then its first n1
+#pragma unroll
+    for (int i = 0; i < 16; ++i) Y[i] = 0.0;
+#pragma unroll
+    for (int c = 0; c < n2; ++c)
+#pragma unroll
+      for (int r = 0; r < m; ++r) Y[r + 4 * c] = X[r + 4 * (n1 + c)];
+#pragma unroll
+    for (int c = 0; c < n1; ++c)
+#pragma unroll
+      for (int r = 0; r < m; ++r) Y[r + 4 * (n2 + c)] = X[r + 4 * c];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) X[i] = Y[i];
+  }
+  double Uq[16], Vr[16];
+  pl_xchg16(X, Y, lane);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { Uq[i] = odd ? Y[i] : X[i]; Vr[i] = odd ? X[i] : Y[i]; }
+  mark(1);
+  // G3 candidates: role 0 (U0, V0), 1 (Uq, V0), 2 (U0, Vr) (role 3 repeats role 0)
+  double Aq[16], Ar[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { Ua[i] = role == 1 ? Uq[i] : U0[i]; Va[i] = role == 2 ? Vr[i] : V0[i]; }
+  pl_congr(Ua, A, Va, Aq, m);
+  pl_congr(Ua, B, Va, Ar, m);
+  const double rq = fmax(pl_lowfro(Aq, n1, n2) / thA, pl_lowfro(Ar, n1, n2) / thB);
+  const double r0 = __shfl_sync(0xffffffffu, rq, gbase), r1 = __shfl_sync(0xffffffffu, rq, gbase + 1),
+               r2 = __shfl_sync(0xffffffffu, rq, gbase + 2);
+  double best = r0;
+  int bi = 0;
+  if (r1 < best) { best = r1; bi = 1; }
+  if (r2 < best) { best = r2; bi = 2; }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    U[i] = bi == 1 ? Uq[i] : U0[i];
+    V[i] = bi == 2 ? Vr[i] : V0[i];
+    An[i] = __shfl_sync(0xffffffffu, Aq[i], gbase + bi);   // = U^T A V, bitwise (same congruence)
+    Bn[i] = __shfl_sync(0xffffffffu, Ar[i], gbase + bi);
+  }
+  if (!(best <= 1.0)) {
+    if (why) { why[0] = 1.0; why[1] = best; }
+    return false;
+  }
+  if (why) { why[0] = 0.0; why[1] = best; }
+  mark(2);
+  const bool ok = pl_swap_tail<N1, N2>(U, V, An, Bn, why);
+  mark(3);
+  if (prof && lane == 0) atomicAdd(&prof[4], 1ull);   // marks taken
+  return ok;
 }
 
 __host__ __device__ inline bool pl_swap(const double* A, const double* B, int n1, int n2, double* U, double* V,
@@ -501,6 +632,32 @@ __device__ __forceinline__ bool pl_transform(const double* Sw, int64_t ldS, cons
   const bool ok = pl_swap_t<N1, N2>(A, B, U, V, An, Bn, why);
 #pragma unroll
   for (int i = 0; i < 16; ++i) { R[i] = U[i]; R[16 + i] = V[i]; R[32 + i] = An[i]; R[48 + i] = Bn[i]; }
+  return ok;
+}
+
+// A group of 4 lanes' transform of a swap of type (N1, N2), N1 + N2 >= 3 (pl_swap_lanes); the
+// lane with `write` stores the record.
+template <int N1, int N2>
+__device__ __forceinline__ bool pl_transform_lanes(const double* Sw, int64_t ldS, const double* Tw, int64_t ldT, int j,
+                                                   double* R, double* why, int lane, bool write,
+                                                   unsigned long long* prof) {
+  constexpr int m = N1 + N2;
+  double A[16], B[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { A[i] = 0.0; B[i] = 0.0; }
+#pragma unroll
+  for (int c = 0; c < m; ++c)
+#pragma unroll
+    for (int r = 0; r < m; ++r) {
+      A[r + 4 * c] = __ldcg(Sw + (j + r) + (int64_t)(j + c) * ldS);
+      B[r + 4 * c] = __ldcg(Tw + (j + r) + (int64_t)(j + c) * ldT);
+    }
+  double U[16], V[16], An[16], Bn[16];
+  const bool ok = pl_swap_lanes<N1, N2>(A, B, U, V, An, Bn, why, lane, prof);
+  if (write) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) { R[i] = U[i]; R[16 + i] = V[i]; R[32 + i] = An[i]; R[48 + i] = Bn[i]; }
+  }
   return ok;
 }
 
@@ -538,6 +695,23 @@ struct PencilWinArgs {
   int32_t force_swap;
   unsigned long long* pprof;   // debug (SN_PPROF): cycles per phase summed over windows, or NULL
 };
+
+// pre[0] = 0, pre[i + 1] = pre[i] + val(i) for i < cnt, by one warp (lane: 0..31)
+template <class F>
+__device__ __forceinline__ void pl_warp_prefix(int* pre, int cnt, int lane, F val) {
+  const int per = (cnt + 31) >> 5, b = lane * per, e = min(b + per, cnt);
+  int local = 0;
+  for (int i = b; i < e; ++i) local += val(i);
+  int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  int run = incl - local;
+  if (lane == 0) pre[0] = 0;
+  for (int i = b; i < e; ++i) { run += val(i); pre[i + 1] = run; }
+}
 
 // index i with pre[i] <= q < pre[i + 1]
 __device__ __forceinline__ int pl_find(const int* pre, int cnt, int q) {
@@ -613,7 +787,8 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   const int32_t* soff = a.step_off + a.step_base[wd.sidx];
   const int nsteps = (int)(a.step_base[wd.sidx + 1] - a.step_base[wd.sidx]) - 1;
   int done_steps = 0;
-  unsigned long long pc[4] = {0, 0, 0, 0};   // transforms, intervals, rows, columns (tid 0, SN_PPROF)
+  unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};   // transforms, intervals, rows, columns, tid 0's own row /
+                                                  // column tasks (tid 0, SN_PPROF)
   long long pk = a.pprof && tid == 0 ? clock64() : 0;
   auto ptick = [&](int q) {
     if (a.pprof && tid == 0) { const long long c = clock64(); pc[q] += (unsigned long long)(c - pk); pk = c; }
@@ -637,39 +812,50 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       for (int t = tp + 1; t <= ty; ++t) s_tstart[t] = i;   // first swap of type >= t
     }
     __syncthreads();
+    // a warp task: 32 swaps of type (1,1) (one per lane), or 8 of another type (a group of 4
+    // lanes per swap, pl_swap_lanes)
     int tbase[5];                                      // first warp task of each type
     tbase[0] = 0;
-    for (int t = 0; t < 4; ++t) tbase[t + 1] = tbase[t] + (((t < 3 ? s_tstart[t + 1] : cnt) - s_tstart[t] + 31) >> 5);
+    for (int t = 0; t < 4; ++t) {
+      const int lg = t == 0 ? 5 : 3;
+      tbase[t + 1] = tbase[t] + (((t < 3 ? s_tstart[t + 1] : cnt) - s_tstart[t] + (1 << lg) - 1) >> lg);
+    }
     for (int i = tid; i < cnt; i += blockDim.x) {
       int t = 0;
       while (t < 3 && s_tstart[t + 1] <= i) ++t;
-      s_owner[i] = (int8_t)((tbase[t] + ((i - s_tstart[t]) >> 5)) % (int)C);
+      s_owner[i] = (int8_t)((tbase[t] + ((i - s_tstart[t]) >> (t == 0 ? 5 : 3))) % (int)C);
     }
+    const int lane = tid & 31;
     for (int g = (tid >> 5) * (int)C + (int)rank; g < tbase[4]; g += (int)(C * (blockDim.x >> 5))) {
       int t = 0;
       while (t < 3 && tbase[t + 1] <= g) ++t;
-      const int i = s_tstart[t] + ((g - tbase[t]) << 5) + (tid & 31);
-      if (i < (t < 3 ? s_tstart[t + 1] : cnt)) {
+      const int tend = t < 3 ? s_tstart[t + 1] : cnt;
+      const int i0 = s_tstart[t] + (t == 0 ? ((g - tbase[t]) << 5) + lane : ((g - tbase[t]) << 3) + (lane >> 2));
+      const bool mine = i0 < tend && (t == 0 || (lane & 3) == 0);   // writes the record
+      const int i = min(i0, tend - 1);               // idle groups repeat a valid swap (no writes)
+      if (t == 0 && i0 >= tend) continue;
+      {
         const int64_t s = s0 + b0 + i;
-        const int j = a.sj[s], n1 = a.s12[s] >> 4, n2 = a.s12[s] & 15;
+        const int j = a.sj[s];
         double* R = rec + i * kRecD;
         double why[2] = {0.0, 0.0};
         bool ok;
         const long long tq0 = a.pprof ? clock64() : 0;
-        if (n1 == 1 && n2 == 1) ok = pl_transform<1, 1>(Sw, ldS, Tw, ldT, j, R, why);
-        else if (n1 == 1) ok = pl_transform<1, 2>(Sw, ldS, Tw, ldT, j, R, why);
-        else if (n2 == 1) ok = pl_transform<2, 1>(Sw, ldS, Tw, ldT, j, R, why);
-        else ok = pl_transform<2, 2>(Sw, ldS, Tw, ldT, j, R, why);
-        if (a.pprof) {   // per-type transform latency (sum, count)
-          const int ty = (n1 - 1) * 2 + (n2 - 1);
-          atomicAdd(&a.pprof[8 + ty], (unsigned long long)(clock64() - tq0));
-          atomicAdd(&a.pprof[12 + ty], 1ull);
-        }
-        if (wd.order == a.force_order && a.sidx[s] == a.force_swap) { ok = false; why[0] = 0.0; }
-        if (ok) atomicMax(&a.ctl->ratio_bits, (unsigned long long)__double_as_longlong(why[1]));
-        if (!ok) {
-          const int key = a.sidx[s];
-          if (atomicMin(&s_rej, key) > key) { s_why[0] = why[0]; s_why[1] = why[1]; }
+        if (t == 0) ok = pl_transform<1, 1>(Sw, ldS, Tw, ldT, j, R, why);
+        else if (t == 1) ok = pl_transform_lanes<1, 2>(Sw, ldS, Tw, ldT, j, R, why, lane, mine, nullptr);
+        else if (t == 2) ok = pl_transform_lanes<2, 1>(Sw, ldS, Tw, ldT, j, R, why, lane, mine, nullptr);
+        else ok = pl_transform_lanes<2, 2>(Sw, ldS, Tw, ldT, j, R, why, lane, mine, a.pprof ? a.pprof + 18 : nullptr);
+        if (mine) {
+          if (a.pprof) {   // per-type transform latency (sum, count)
+            atomicAdd(&a.pprof[8 + t], (unsigned long long)(clock64() - tq0));
+            atomicAdd(&a.pprof[12 + t], 1ull);
+          }
+          if (wd.order == a.force_order && a.sidx[s] == a.force_swap) { ok = false; why[0] = 0.0; }
+          if (ok) atomicMax(&a.ctl->ratio_bits, (unsigned long long)__double_as_longlong(why[1]));
+          if (!ok) {
+            const int key = a.sidx[s];
+            if (atomicMin(&s_rej, key) > key) { s_why[0] = why[0]; s_why[1] = why[1]; }
+          }
         }
       }
     }
@@ -708,13 +894,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       s_lo[tid] = (int16_t)lo;
       s_hi[tid] = (int16_t)hi;
     }
-    if (tid == 0) {
-      s_pre[0] = 0;
-      for (int i = 0; i < cnt; ++i) {
-        const int j = s_j[i], m = s_m[i];
-        s_pre[i + 1] = s_pre[i] + 2 * (k - j - m);
-      }
-    }
+    if (tid < 32) pl_warp_prefix(s_pre, cnt, tid, [&](int i) { return 2 * (k - s_j[i] - s_m[i]); });
     __syncthreads();
     ptick(1);
     // (3) rows j..j+m-1 right of each block (S, T); the new diagonal blocks
@@ -763,19 +943,20 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
       if (phase == 1) {
         csync();   // row applications (all CTAs) before column applications (corner order)
         ptick(2);
-        if (tid == 0)
-          for (int i = 0; i < cnt; ++i) s_pre[i + 1] = s_pre[i] + 2 * s_j[i] + 2 * (s_hi[i] - s_lo[i] + 1);
+        if (tid < 32) pl_warp_prefix(s_pre, cnt, tid, [&](int i) { return 2 * s_j[i] + 2 * (s_hi[i] - s_lo[i] + 1); });
         __syncthreads();
       }
       const int total = s_pre[cnt];
-      for (int q0 = gt; q0 < total; q0 += 2 * GC) {
-        double* X[2];
-        int64_t base[2], stride[2];
-        const double* G[2];
-        int m[2];
-        double x[2][4];
+      constexpr int NU = 4;   // tasks per thread and round: their loads are all in flight at once
+      const long long lq0 = a.pprof && tid == 0 ? clock64() : 0;
+      for (int q0 = gt; q0 < total; q0 += NU * GC) {
+        double* X[NU];
+        int64_t base[NU], stride[NU];
+        const double* G[NU];
+        int m[NU];
+        double x[NU][4];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < NU; ++u) {
           const int q = q0 + u * GC;
           m[u] = 0;
           if (q < total) {
@@ -786,7 +967,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
           for (int t = 0; t < 4; ++t) x[u][t] = t < m[u] ? __ldcg(X[u] + base[u] + t * stride[u]) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < NU; ++u) {
           double y[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
@@ -800,6 +981,7 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
             if (t < m[u]) X[u][base[u] + t * stride[u]] = y[t];
         }
       }
+      if (a.pprof && tid == 0) pc[4 + phase] += (unsigned long long)(clock64() - lq0);   // tid 0's own tasks
     }
     done_steps = st + 1;
     csync();
@@ -807,6 +989,8 @@ __global__ void __launch_bounds__(256) pencil_window_kernel(PencilWinArgs a) {
   }
   if (a.pprof && tid == 0 && rank == 0) {
     for (int q = 0; q < 4; ++q) atomicAdd(&a.pprof[q], pc[q]);
+    atomicAdd(&a.pprof[16], pc[4]);
+    atomicAdd(&a.pprof[17], pc[5]);
     atomicAdd(&a.pprof[4], (unsigned long long)nsteps);
     atomicAdd(&a.pprof[5], 1ull);
     atomicAdd(&a.pprof[6], (unsigned long long)(soff[nsteps] - soff[0]));
@@ -1023,8 +1207,8 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
     if (Q) panel_maps_init(&mQ, (double*)dUL.p, maxper, Q, n, n, ldQ);
     if (Zm) panel_maps_init(&mZ, (double*)dVR.p, maxper, Zm, n, n, ldZ);
     if (std::getenv("SN_PPROF")) {
-      PK(dpprof.alloc(16 * sizeof(unsigned long long)));
-      PK(cudaMemsetAsync(dpprof.p, 0, 16 * sizeof(unsigned long long), sA));
+      PK(dpprof.alloc(24 * sizeof(unsigned long long)));
+      PK(cudaMemsetAsync(dpprof.p, 0, 24 * sizeof(unsigned long long), sA));
     }
     PK(cudaEventCreate(&e0));
     PK(cudaEventCreate(&e1));
@@ -1111,18 +1295,20 @@ int run_pencil(const sn_opts& o, int64_t n, double* S, int64_t ldS, double* T, i
     PK(cudaMemcpy(hdone.data(), ddone.p, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost));
     PK(cudaMemcpy(&hctl, dctl.p, sizeof(Control), cudaMemcpyDeviceToHost));
     if (dpprof.p) {
-      unsigned long long h[16];
+      unsigned long long h[24];
       PK(cudaMemcpy(h, dpprof.p, sizeof(h), cudaMemcpyDeviceToHost));
       const double w = h[5] ? (double)h[5] : 1.0;
       double lat[4];
       for (int q = 0; q < 4; ++q) lat[q] = h[12 + q] ? (double)h[8 + q] / (double)h[12 + q] : 0.0;
+      const double c22 = h[22] ? (double)h[22] : 1.0;   // warps that marked (lane 0)
       std::fprintf(stderr,
                    "{\"probe\": \"pencil_window_phases\", \"windows\": %llu, \"steps_per_window\": %.1f, "
                    "\"swaps_per_window\": %.1f, \"cycles_per_window\": {\"transform\": %.0f, \"intervals\": %.0f, "
                    "\"rows\": %.0f, \"cols\": %.0f}, \"transform_cycles_by_type\": [%.0f, %.0f, %.0f, %.0f], "
-                   "\"swaps_by_type\": [%llu, %llu, %llu, %llu]}\n",
+                   "\"swaps_by_type\": [%llu, %llu, %llu, %llu], \"own_task_cycles\": {\"rows\": %.0f, \"cols\": %.0f}, "
+                   "\"swap22_cumulative_cycles\": {\"sylvester\": %.0f, \"bases\": %.0f, \"candidates\": %.0f, \"all\": %.0f}}\n",
                    h[5], h[4] / w, h[6] / w, h[0] / w, h[1] / w, h[2] / w, h[3] / w, lat[0], lat[1], lat[2], lat[3],
-                   h[12], h[13], h[14], h[15]);
+                   h[12], h[13], h[14], h[15], h[16] / w, h[17] / w, h[18] / c22, h[19] / c22, h[20] / c22, h[21] / c22);
     }
   }
   {
