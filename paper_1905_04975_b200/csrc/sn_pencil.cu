@@ -240,6 +240,155 @@ __host__ __device__ __forceinline__ void pl_gsylv(const double* A, const double*
     }
 }
 
+// pl_gsylv by a group of 4 lanes (all 32 lanes of the warp call it; lane & 3 = role): the same
+// Kronecker system, pivots, eliminations and back substitution, so the same R and L.  Role q
+// holds K/4 rows of the system (physical rows q K/4 ..); row exchanges are tracked as logical
+// positions instead of moving rows, column exchanges are made in every row as in pl_gsylv.  The
+// complete-pivoting search is a per-lane scan plus a two-step shuffle reduction with
+// pl_gsylv's tie rule (the first maximum in row-major order of the active submatrix); the
+// pivot row and every back-substituted unknown are broadcast by the lane that holds them.
+template <int N1, int N2>
+__device__ __forceinline__ void pl_gsylv_lanes(const double* A, const double* B, double* R, double* L, int lane) {
+  constexpr int N = N1 * N2, K = 2 * N, RPL = K / 4;
+  const int q = lane & 3, gbase = lane & ~3;
+  double M[RPL][K], y[RPL];
+  int lpos[RPL];
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    lpos[k] = q * RPL + k;
+#pragma unroll
+    for (int c = 0; c < K; ++c) M[k][c] = 0.0;
+    y[k] = 0.0;
+  }
+  // rows of the system (pl_gsylv's construction: every entry is set once)
+#pragma unroll
+  for (int jj = 0; jj < N2; ++jj)
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      const int e = i + N1 * jj;
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        const int rho = q * RPL + k;
+        if (rho == e || rho == N + e) {
+          const double* X = rho == e ? A : B;
+#pragma unroll
+          for (int l = 0; l < N1; ++l) M[k][l + N1 * jj] = 0.0 + X[i + 4 * l];
+#pragma unroll
+          for (int l = 0; l < N2; ++l) M[k][N + i + N1 * l] = 0.0 - X[(N1 + l) + 4 * (N1 + jj)];
+          y[k] = X[i + 4 * (N1 + jj)];
+        }
+      }
+    }
+  double mx = 0.0;
+#pragma unroll
+  for (int k = 0; k < RPL; ++k)
+#pragma unroll
+    for (int c = 0; c < K; ++c) mx = fmax(mx, fabs(M[k][c]));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+  mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+  const double smin = fmax(2.220446049250313e-16 * mx, 2.2250738585072014e-308 / 2.220446049250313e-16);
+  int cp[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) cp[c] = c;
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    // this lane's candidate, then the group's: larger |v|, ties to the smaller (row, column)
+    double bv = -1.0;
+    int br = K, bc = K;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k)
+#pragma unroll
+      for (int c = p; c < K; ++c) {
+        const double v = fabs(M[k][c]);
+        const bool ok = lpos[k] >= p && (v > bv || (v == bv && (lpos[k] < br || (lpos[k] == br && c < bc))));
+        if (ok) { bv = v; br = lpos[k]; bc = c; }
+      }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, br, o), oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (ov > bv || (ov == bv && (orr < br || (orr == br && oc < bc)))) { bv = ov; br = orr; bc = oc; }
+    }
+    const int pr = br < K ? br : p, pc = br < K ? bc : p;
+    // row exchange p <-> pr (logical positions)
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      if (pr != p) {
+        if (lpos[k] == p) lpos[k] = pr;
+        else if (lpos[k] == pr) lpos[k] = p;
+      }
+    }
+    // column exchange p <-> pc in every row
+#pragma unroll
+    for (int c = p + 1; c < K; ++c)
+      if (c == pc) {
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) { const double t = M[k][p]; M[k][p] = M[k][c]; M[k][c] = t; }
+        const int t = cp[p]; cp[p] = cp[c]; cp[c] = t;
+      }
+    // the pivot row (clamped pivot) from the lane that holds logical row p
+    double prow[K], py = 0.0;
+#pragma unroll
+    for (int c = 0; c < K; ++c) prow[c] = 0.0;
+    bool has = false;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k)
+      if (lpos[k] == p) {
+        has = true;
+        if (fabs(M[k][p]) < smin) M[k][p] = smin;
+#pragma unroll
+        for (int c = p; c < K; ++c) prow[c] = M[k][c];
+        py = y[k];
+      }
+    const unsigned own = (__ballot_sync(0xffffffffu, has) >> gbase) & 0xFu;
+    const int src = gbase + __ffs(own) - 1;
+#pragma unroll
+    for (int c = p; c < K; ++c) prow[c] = __shfl_sync(0xffffffffu, prow[c], src);
+    py = __shfl_sync(0xffffffffu, py, src);
+    const double ip = 1.0 / prow[p];
+#pragma unroll
+    for (int k = 0; k < RPL; ++k)
+      if (lpos[k] > p) {
+        const double f = M[k][p] * ip;
+#pragma unroll
+        for (int c = p; c < K; ++c) M[k][c] -= f * prow[c];
+        y[k] -= f * py;
+      }
+  }
+  double z[K], x[K];
+#pragma unroll
+  for (int p = K - 1; p >= 0; --p) {
+    double zp = 0.0;
+    bool has = false;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k)
+      if (lpos[k] == p) {
+        has = true;
+        double acc = y[k];
+#pragma unroll
+        for (int c = p + 1; c < K; ++c) acc -= M[k][c] * z[c];
+        zp = acc / M[k][p];
+      }
+    const unsigned own = (__ballot_sync(0xffffffffu, has) >> gbase) & 0xFu;
+    z[p] = __shfl_sync(0xffffffffu, zp, gbase + __ffs(own) - 1);
+  }
+#pragma unroll
+  for (int qq = 0; qq < K; ++qq) {
+    double v = 0.0;
+#pragma unroll
+    for (int p = 0; p < K; ++p)
+      if (cp[p] == qq) v = z[p];
+    x[qq] = v;
+  }
+#pragma unroll
+  for (int jj = 0; jj < N2; ++jj)
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      R[i + 2 * jj] = x[i + N1 * jj];
+      L[i + 2 * jj] = x[N + i + N1 * jj];
+    }
+}
+
 // Frobenius norm of the n1 x n2 block below the leading n2 x n2 block (G3)
 __host__ __device__ __forceinline__ double pl_lowfro(const double* X, int n1, int n2) {
   double acc = 0.0;
@@ -516,7 +665,7 @@ __device__ bool pl_swap_lanes(const double* A, const double* B, double* U, doubl
   const double eps = 2.220446049250313e-16, sml = 2.2250738585072014e-308 / 2.220446049250313e-16;
   const double thA = fmax(kG3C * eps * anorm, sml), thB = fmax(kG3C * eps * bnorm, sml);
   double R[4] = {0.0, 0.0, 0.0, 0.0}, L[4] = {0.0, 0.0, 0.0, 0.0};
-  pl_gsylv<N1, N2>(A, B, R, L);
+  pl_gsylv_lanes<N1, N2>(A, B, R, L, lane);
   mark(0);
   // Sylvester bases: even lanes V0 = basis of span[-R; I], odd lanes U0 = basis of span[-L; I]
   double M[16], X[16], Y[16], U0[16], V0[16];

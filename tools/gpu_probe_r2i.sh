@@ -1,0 +1,14 @@
+#!/bin/bash
+# Round-2 probe call i: pencil applications by 32-task warp units;
+# pencil GPU tests, phase timing.
+set -u
+cd "$(dirname "$0")/.."
+TAG=${1:-r2i}
+O=gpurun_out/$TAG
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+for c in 1 2; do
+  SN_PPROF=1 timeout 600 python tools/bench_pencil.py --config $c --steps 2 --warmup 1 > $O/pencil_c$c.log 2>&1
+done
+timeout 1200 python -m pytest tests/test_gpu_pencil.py -x -q > $O/pytest_pencil.log 2>&1; echo "pytest rc=$?" >> $O/pytest_pencil.log
+tail -3 $O/pytest_pencil.log; grep -h '^{' $O/pencil_*.log

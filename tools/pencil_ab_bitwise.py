@@ -22,7 +22,7 @@ def main():
     for n, w, p2, seed in ((700, 256, 0.25, 7), (2000, 128, 0.5, 12), (4096, 128, 0.25, 1)):
         p = make_pencil(n, p2=p2, q="householder", psel=0.35, w=w, seed=seed, device="cuda")
         S, T, Q, Z = p.S.clone(), p.T.clone(), p.Q.clone(), p.Z.clone()
-        kw = {} if "base" in os.environ.get("SN_LIB_PATH", "") else {"pencil_cluster": cl}
+        kw = {} if os.environ.get("SN_LIB_PATH", "").endswith("_base.so") else {"pencil_cluster": cl}
         r = sn.reorder_pencil(S, T, Q, Z, p.select, window=w, **kw)
         torch.cuda.synchronize()
         assert r["rc"] == 0, r["rc"]
