@@ -18,7 +18,12 @@
 namespace sn {
 namespace {
 
-constexpr int kThreads = 256;   // 4 transform warps + 4 apply warps (the DMMA tiles use warps 0-7)
+#ifndef SN_WIN_THREADS
+#define SN_WIN_THREADS 256
+#endif
+// 4 transform warps + (kThreads/32 - 4) apply warps (the DMMA tiles use warps 0-7)
+constexpr int kThreads = SN_WIN_THREADS;
+static_assert(kThreads % 32 == 0 && kThreads >= 256, "window kernel needs >= 8 warps");
 constexpr int LDD = 65;   // inner window (odd stride: conflict-free row walks)
 constexpr int LDZ = 68;   // inner accumulator (== 4 mod 16: conflict-free DMMA fragments)
 constexpr int LDT = 68;   // staging tile
@@ -141,6 +146,10 @@ __device__ void inner_update(double* P, int64_t ld, int64_t r0, int64_t c0, int 
 // columns of mover i's step-t pair, which only mover i's step-t column application changes:
 // the transform thread applies that column transform to those rows itself (and writes them
 // back), and the apply warps skip them.  One CTA barrier per step.
+#ifndef SN_WIN_QUAD
+#define SN_WIN_QUAD 0
+#endif
+constexpr int kG22 = SN_WIN_QUAD ? 4 : 2;  // lanes per 2x2|2x2 transform (quad: lane-parallel Sylvester)
 constexpr int kWT = 4;                     // transform warps: w < 3 swap type w, w = 3 2x2|2x2
 constexpr int kWA = kThreads / 32 - kWT;   // apply warps
 constexpr int kRecBuf = 4 * 32 * dev::kRec;   // doubles per record buffer (type x slot)
@@ -304,8 +313,8 @@ __device__ void wave_transform(int t, int base, double* Din, double* recs, WaveS
     }
   } else if (warp == 3) {
     const int c3 = W.cnt[sb][3];
-    for (int b0 = 0; b0 < c3; b0 += 16) {
-      const int slot = b0 + (lane >> 1), role = lane & 1;
+    for (int b0 = 0; b0 < c3; b0 += 32 / kG22) {
+      const int slot = b0 + lane / kG22, role = lane % kG22;
       const bool act = slot < c3;
       const int sl = act ? slot : b0;
       const int j = W.lj[sb][3][sl];
@@ -317,7 +326,7 @@ __device__ void wave_transform(int t, int base, double* Din, double* recs, WaveS
       if (act && role == 0 && nw) wave_writeback<2>(jp, pnd, j, Din, cpl);
       double tmp[dev::kGen];
       const long long q1 = g_tprof_on ? clock64() : 0;
-      bool rj = dev::swap_compute_22_paired_blk(Db, tmp, role);
+      bool rj = kG22 == 4 ? dev::swap_compute_22_quad_blk(Db, tmp, role) : dev::swap_compute_22_paired_blk(Db, tmp, role);
       if (g_tprof_on) atomicMax(&W.tmax[3], (unsigned long long)(clock64() - q1));
       if (act && role == 0) {
         rj = rj || (force_here && (base + flat == force_swap));
